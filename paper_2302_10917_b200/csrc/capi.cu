@@ -1,0 +1,430 @@
+// The C-ABI of libmehdg_b200.so: system lifecycle, uploads, factorisation
+// and the operator entry points.  See include/mehdg_b200.h for the mapping
+// to the reference functions (schur_solver.py).
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "mh_internal.h"
+
+namespace mh {
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+}  // namespace mh
+
+using namespace mh;
+
+extern "C" const char* mh_last_error(void) { return g_err.c_str(); }
+extern "C" int mh_version(void) { return 1; }
+
+extern "C" int mh_device_count(int* count) {
+  if (!count) return MH_E_ARG;
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    c = 0;
+  }
+  *count = c;
+  return MH_OK;
+}
+
+static int need(mh_system* s, bool cond, const char* msg) {
+  if (!s) {
+    set_error("null system");
+    return MH_E_ARG;
+  }
+  if (!cond) {
+    set_error(msg);
+    return MH_E_STATE;
+  }
+  return MH_OK;
+}
+
+extern "C" int mh_create(int device, int nfe, int64_t n_elem, int q, int t, int64_t n_face,
+                         mh_system** out) {
+  if (!out || nfe < 1 || nfe > 4 || n_elem < 0 || q < 1 || t < 1 || n_face < 0) {
+    set_error("mh_create: bad sizes");
+    return MH_E_ARG;
+  }
+  if (q > 256 || t > 128) {
+    set_error("mh_create: Q <= 256 and t <= 128 are supported");
+    return MH_E_UNSUPPORTED;
+  }
+  *out = nullptr;
+  MH_CHECK_CUDA(cudaSetDevice(device));
+  mh_system* s = new mh_system();
+  s->device = device;
+  s->nfe = nfe;
+  s->N = n_elem;
+  s->Q = q;
+  s->t = t;
+  s->nc = nfe * t;
+  s->F = n_face;
+  cudaDeviceGetAttribute(&s->max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, device);
+  cudaError_t e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete s;
+    set_error(std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
+    return MH_E_CUDA;
+  }
+  s->own_stream = true;
+  *out = s;
+  return MH_OK;
+}
+
+extern "C" int mh_destroy(mh_system* s) {
+  if (!s) return MH_OK;
+  cudaSetDevice(s->device);
+  if (s->stream) cudaStreamSynchronize(s->stream);
+  s->elem_ufac.release(); s->face_vslot.release();
+  s->A.release(); s->LU.release(); s->dinv.release(); s->piv.release(); s->perm.release();
+  s->lstat.release(); s->Bt.release(); s->Cm.release(); s->Ru.release(); s->D.release();
+  s->Draw.release(); s->Rhat.release(); s->FL.release(); s->FU.release(); s->FrL.release();
+  s->FrU.release(); s->Fperm.release(); s->Fsign.release(); s->Fkind.release(); s->V.release();
+  s->tmp.release(); s->S.release(); s->halo_u.release(); s->hin.release(); s->hout.release();
+  if (s->kry) free_krylov(s->kry);
+  free_comm(s);
+  if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
+  delete s;
+  return MH_OK;
+}
+
+extern "C" int mh_set_stream(mh_system* s, void* stream) {
+  if (!s) return MH_E_ARG;
+  if (s->own_stream && s->stream) {
+    cudaStreamSynchronize(s->stream);
+    cudaStreamDestroy(s->stream);
+  }
+  s->stream = (cudaStream_t)stream;
+  s->own_stream = false;
+  return MH_OK;
+}
+
+extern "C" int mh_upload_connectivity(mh_system* s, const int32_t* elem_ufac,
+                                      const int32_t* face_elem, const int32_t* face_slot) {
+  if (!s || (s->N > 0 && !elem_ufac) || (s->F > 0 && (!face_elem || !face_slot))) {
+    set_error("mh_upload_connectivity: null argument");
+    return MH_E_ARG;
+  }
+  MH_CHECK_CUDA(cudaSetDevice(s->device));
+  const int64_t ntrace = s->F + s->F_halo;
+  for (int64_t i = 0; i < s->N * s->nfe; ++i)
+    if (elem_ufac[i] < -1 || elem_ufac[i] >= ntrace) {
+      set_error("elem_ufac entry out of range");
+      return MH_E_ARG;
+    }
+  std::vector<int32_t> vslot((size_t)(2 * s->F));
+  for (int64_t f = 0; f < s->F; ++f)
+    for (int c = 0; c < 2; ++c) {
+      const int32_t e = face_elem[2 * f + c], k = face_slot[2 * f + c];
+      if (e < 0) {
+        vslot[2 * f + c] = -1;
+        continue;
+      }
+      if (e >= s->N + s->n_vslot_extra || k < 0 || k >= s->nfe) {
+        set_error("face table entry out of range");
+        return MH_E_ARG;
+      }
+      // e >= N addresses a received v-slot segment (multi-GPU halo)
+      vslot[2 * f + c] = e < s->N ? (int32_t)(e * s->nfe + k)
+                                  : (int32_t)(s->N * s->nfe + (e - s->N));
+    }
+  s->h_face_elem.assign(face_elem, face_elem + 2 * s->F);
+  s->h_face_slot.assign(face_slot, face_slot + 2 * s->F);
+  MH_CHECK(s->elem_ufac.alloc((size_t)(s->N * s->nfe)));
+  MH_CHECK(s->face_vslot.alloc((size_t)(2 * s->F)));
+  if (s->N)
+    MH_CHECK_CUDA(cudaMemcpyAsync(s->elem_ufac.p, elem_ufac, sizeof(int32_t) * s->N * s->nfe,
+                                  cudaMemcpyHostToDevice, s->stream));
+  if (s->F)
+    MH_CHECK_CUDA(cudaMemcpyAsync(s->face_vslot.p, vslot.data(), sizeof(int32_t) * 2 * s->F,
+                                  cudaMemcpyHostToDevice, s->stream));
+  MH_CHECK_CUDA(cudaStreamSynchronize(s->stream));
+  s->have_conn = true;
+  return MH_OK;
+}
+
+static int alloc_blocks(mh_system* s) {
+  const size_t N = (size_t)s->N, Q = s->Q, nc = s->nc, F = (size_t)s->F, t = s->t;
+  MH_CHECK(s->A.alloc(N * Q * Q));
+  MH_CHECK(s->LU.alloc(N * Q * Q));
+  MH_CHECK(s->dinv.alloc(N * Q));
+  MH_CHECK(s->piv.alloc(N * Q));
+  MH_CHECK(s->perm.alloc(N * Q));
+  MH_CHECK(s->lstat.alloc(N));
+  MH_CHECK(s->Bt.alloc(N * nc * Q));
+  MH_CHECK(s->Ru.alloc(N * Q));
+  MH_CHECK(s->D.alloc(F * t * t));
+  MH_CHECK(s->Draw.alloc(F * t * t));
+  MH_CHECK(s->Rhat.alloc(F * t));
+  MH_CHECK(s->FL.alloc(F * t * t));
+  MH_CHECK(s->FU.alloc(F * t * t));
+  MH_CHECK(s->FrL.alloc(F * t));
+  MH_CHECK(s->FrU.alloc(F * t));
+  MH_CHECK(s->Fperm.alloc(F * t));
+  MH_CHECK(s->Fsign.alloc(F));
+  MH_CHECK(s->Fkind.alloc(F));
+  MH_CHECK(s->V.alloc((N * s->nfe + (size_t)s->n_vslot_extra) * t));
+  MH_CHECK(s->tmp.alloc((F + (size_t)s->F_halo) * t + 1));
+  return MH_OK;
+}
+
+static int upload_impl(mh_system* s, const double* A, const double* B, const double* C,
+                       const double* Ru, const double* D, const double* Rhat,
+                       cudaMemcpyKind kind) {
+  if (!s || (s->N > 0 && !A) || (s->N > 0 && !B && !C) || (s->F > 0 && !D)) {
+    set_error("mh_upload_blocks: null argument");
+    return MH_E_ARG;
+  }
+  MH_CHECK_CUDA(cudaSetDevice(s->device));
+  MH_CHECK(alloc_blocks(s));
+  const size_t N = (size_t)s->N, Q = s->Q, nc = s->nc, F = (size_t)s->F, t = s->t;
+  cudaStream_t st = s->stream;
+  if (N) MH_CHECK_CUDA(cudaMemcpyAsync(s->A.p, A, sizeof(double) * N * Q * Q, kind, st));
+  s->c_is_bt = (B == nullptr) || (C == nullptr);
+  if (!s->c_is_bt) MH_CHECK(s->Cm.alloc(N * nc * Q));
+  else s->Cm.release();
+  if (B == nullptr) {
+    if (N) MH_CHECK_CUDA(cudaMemcpyAsync(s->Bt.p, C, sizeof(double) * N * nc * Q, kind, st));
+  } else {
+    // op.B (N x Q x nc) -> Bt (N x nc x Q), staged through LU's storage
+    if (N) {
+      double* stage = s->LU.p;
+      if (nc > Q) {  // LU slot is too small: use a temporary
+        MH_CHECK(s->S.alloc(N * nc * Q));
+        stage = s->S.p;
+      }
+      MH_CHECK_CUDA(cudaMemcpyAsync(stage, B, sizeof(double) * N * nc * Q, kind, st));
+      MH_CHECK(launch_transpose_batched(st, stage, s->Bt.p, (int64_t)N, (int)Q, (int)nc));
+      MH_CHECK_CUDA(cudaStreamSynchronize(st));
+      if (stage == s->S.p) s->S.release();
+    }
+    if (C && N) MH_CHECK_CUDA(cudaMemcpyAsync(s->Cm.p, C, sizeof(double) * N * nc * Q, kind, st));
+  }
+  if (N) {
+    if (Ru) MH_CHECK_CUDA(cudaMemcpyAsync(s->Ru.p, Ru, sizeof(double) * N * Q, kind, st));
+    else MH_CHECK_CUDA(cudaMemsetAsync(s->Ru.p, 0, sizeof(double) * N * Q, st));
+  }
+  if (F) {
+    MH_CHECK_CUDA(cudaMemcpyAsync(s->Draw.p, D, sizeof(double) * F * t * t, kind, st));
+    if (Rhat) MH_CHECK_CUDA(cudaMemcpyAsync(s->Rhat.p, Rhat, sizeof(double) * F * t, kind, st));
+    else MH_CHECK_CUDA(cudaMemsetAsync(s->Rhat.p, 0, sizeof(double) * F * t, st));
+  }
+  MH_CHECK_CUDA(cudaMemsetAsync(s->V.p, 0, sizeof(double) * s->V.n, st));
+  MH_CHECK_CUDA(cudaStreamSynchronize(st));
+  s->have_blocks = true;
+  s->factored = false;
+  s->have_mb = false;
+  return MH_OK;
+}
+
+extern "C" int mh_upload_blocks(mh_system* s, const double* A, const double* B, const double* C,
+                                const double* Ru, const double* D, const double* Rhat) {
+  return upload_impl(s, A, B, C, Ru, D, Rhat, cudaMemcpyHostToDevice);
+}
+
+extern "C" int mh_upload_blocks_device(mh_system* s, const double* A, const double* B,
+                                       const double* C, const double* Ru, const double* D,
+                                       const double* Rhat) {
+  return upload_impl(s, A, B, C, Ru, D, Rhat, cudaMemcpyDeviceToDevice);
+}
+
+extern "C" int mh_factorize(mh_system* s, int32_t* fail_macro, int32_t* fail_face,
+                            int8_t* face_kinds, float* lu_ms) {
+  MH_CHECK(need(s, s && s->have_blocks, "mh_factorize before mh_upload_blocks"));
+  MH_CHECK_CUDA(cudaSetDevice(s->device));
+  if (fail_macro) *fail_macro = -1;
+  if (fail_face) *fail_face = -1;
+  MH_CHECK(launch_lu(s, lu_ms));
+  MH_CHECK(launch_face_factor(s, s->Draw.p));
+  std::vector<int32_t> st((size_t)s->N);
+  std::vector<int8_t> kinds((size_t)s->F);
+  if (s->N)
+    MH_CHECK_CUDA(cudaMemcpyAsync(st.data(), s->lstat.p, sizeof(int32_t) * s->N,
+                                  cudaMemcpyDeviceToHost, s->stream));
+  if (s->F)
+    MH_CHECK_CUDA(cudaMemcpyAsync(kinds.data(), s->Fkind.p, s->F, cudaMemcpyDeviceToHost,
+                                  s->stream));
+  MH_CHECK_CUDA(cudaStreamSynchronize(s->stream));
+  if (face_kinds && s->F) std::memcpy(face_kinds, kinds.data(), s->F);
+  // the reference factorises all macros before any face (schur_solver.py:195-196)
+  for (int64_t e = 0; e < s->N; ++e)
+    if (st[e]) {
+      if (fail_macro) *fail_macro = (int32_t)e;
+      set_error("singular local block");
+      return MH_E_SINGULAR_LOCAL;
+    }
+  for (int64_t f = 0; f < s->F; ++f)
+    if (kinds[f] == MH_FACE_SINGULAR) {
+      if (fail_face) *fail_face = (int32_t)f;
+      set_error("singular face block");
+      return MH_E_SINGULAR_FACE;
+    }
+  s->factored = true;
+  return MH_OK;
+}
+
+extern "C" int mh_refactorize_local(mh_system* s, float* lu_ms) {
+  MH_CHECK(need(s, s && s->have_blocks, "mh_refactorize_local before upload"));
+  MH_CHECK_CUDA(cudaSetDevice(s->device));
+  return launch_lu(s, lu_ms);
+}
+
+extern "C" int mh_get_local_factors(mh_system* s, int64_t first, int64_t count, double* lu_host,
+                                    int32_t* piv_host) {
+  MH_CHECK(need(s, s && s->factored, "factors requested before mh_factorize"));
+  if (first < 0 || count < 0 || first + count > s->N) {
+    set_error("macro range out of bounds");
+    return MH_E_ARG;
+  }
+  MH_CHECK_CUDA(cudaSetDevice(s->device));
+  const size_t QQ = (size_t)s->Q * s->Q;
+  if (lu_host && count) {
+    DBuf<double> tmp;
+    MH_CHECK(tmp.alloc(QQ * count));
+    // column-major device factors -> row-major host (scipy's lu[i, j])
+    MH_CHECK(launch_transpose_batched(s->stream, s->LU.p + first * QQ, tmp.p, count, s->Q, s->Q));
+    MH_CHECK_CUDA(cudaMemcpyAsync(lu_host, tmp.p, sizeof(double) * QQ * count,
+                                  cudaMemcpyDeviceToHost, s->stream));
+    MH_CHECK_CUDA(cudaStreamSynchronize(s->stream));
+    tmp.release();
+  }
+  if (piv_host && count)
+    MH_CHECK_CUDA(cudaMemcpyAsync(piv_host, s->piv.p + first * s->Q,
+                                  sizeof(int32_t) * s->Q * count, cudaMemcpyDeviceToHost,
+                                  s->stream));
+  MH_CHECK_CUDA(cudaStreamSynchronize(s->stream));
+  return MH_OK;
+}
+
+// ---- operator ---------------------------------------------------------------
+
+static int ready(mh_system* s) {
+  MH_CHECK(need(s, s && s->have_conn, "connectivity not uploaded"));
+  MH_CHECK(need(s, s->factored, "system not factorised (mh_factorize)"));
+  return MH_OK;
+}
+
+extern "C" int mh_rhs(mh_system* s, double* f) {
+  MH_CHECK(ready(s));
+  MH_CHECK(halo_rhs_begin(s));
+  MH_CHECK(launch_element(s, kRhs, nullptr, s->V.p));
+  MH_CHECK(halo_v_exchange(s));
+  return launch_face_reduce(s, nullptr, f, 1, 0);
+}
+
+extern "C" int mh_apply(mh_system* s, const double* u, double* w) {
+  MH_CHECK(ready(s));
+  MH_CHECK(halo_u_exchange(s, u, nullptr));
+  MH_CHECK(launch_element(s, kApply, u, s->V.p));
+  MH_CHECK(halo_v_exchange(s));
+  return launch_face_reduce(s, u, w, 0, 0);
+}
+
+extern "C" int mh_apply_precond(mh_system* s, const double* u, double* z) {
+  MH_CHECK(ready(s));
+  MH_CHECK(halo_u_exchange(s, u, nullptr));
+  MH_CHECK(launch_element(s, kApply, u, s->V.p));
+  MH_CHECK(halo_v_exchange(s));
+  return launch_face_reduce(s, u, z, 0, 1);
+}
+
+extern "C" int mh_precond(mh_system* s, const double* w, double* z) {
+  MH_CHECK(ready(s));
+  return launch_precond(s, w, z);
+}
+
+extern "C" int mh_reconstruct(mh_system* s, const double* u, double* U) {
+  MH_CHECK(ready(s));
+  MH_CHECK(halo_u_exchange(s, u, nullptr));
+  return launch_element(s, kRecon, u, U);
+}
+
+static int host_io(mh_system* s, size_t nin, size_t nout) {
+  MH_CHECK(s->hin.alloc(std::max<size_t>(nin, 1)));
+  MH_CHECK(s->hout.alloc(std::max<size_t>(nout, 1)));
+  return MH_OK;
+}
+
+extern "C" int mh_apply_host(mh_system* s, const double* u, double* w) {
+  MH_CHECK(ready(s));
+  const size_t n = (size_t)(s->F * s->t);
+  MH_CHECK(host_io(s, n, n));
+  MH_CHECK_CUDA(cudaMemcpyAsync(s->hin.p, u, n * 8, cudaMemcpyHostToDevice, s->stream));
+  MH_CHECK(mh_apply(s, s->hin.p, s->hout.p));
+  MH_CHECK_CUDA(cudaMemcpyAsync(w, s->hout.p, n * 8, cudaMemcpyDeviceToHost, s->stream));
+  MH_CHECK_CUDA(cudaStreamSynchronize(s->stream));
+  return MH_OK;
+}
+
+extern "C" int mh_precond_host(mh_system* s, const double* w, double* z) {
+  MH_CHECK(ready(s));
+  const size_t n = (size_t)(s->F * s->t);
+  MH_CHECK(host_io(s, n, n));
+  MH_CHECK_CUDA(cudaMemcpyAsync(s->hin.p, w, n * 8, cudaMemcpyHostToDevice, s->stream));
+  MH_CHECK(mh_precond(s, s->hin.p, s->hout.p));
+  MH_CHECK_CUDA(cudaMemcpyAsync(z, s->hout.p, n * 8, cudaMemcpyDeviceToHost, s->stream));
+  MH_CHECK_CUDA(cudaStreamSynchronize(s->stream));
+  return MH_OK;
+}
+
+extern "C" int mh_rhs_host(mh_system* s, double* f) {
+  MH_CHECK(ready(s));
+  const size_t n = (size_t)(s->F * s->t);
+  MH_CHECK(host_io(s, 1, n));
+  MH_CHECK(mh_rhs(s, s->hout.p));
+  MH_CHECK_CUDA(cudaMemcpyAsync(f, s->hout.p, n * 8, cudaMemcpyDeviceToHost, s->stream));
+  MH_CHECK_CUDA(cudaStreamSynchronize(s->stream));
+  return MH_OK;
+}
+
+extern "C" int mh_reconstruct_host(mh_system* s, const double* u, double* U) {
+  MH_CHECK(ready(s));
+  const size_t n = (size_t)(s->F * s->t), nU = (size_t)s->N * s->Q;
+  MH_CHECK(host_io(s, n, nU));
+  MH_CHECK_CUDA(cudaMemcpyAsync(s->hin.p, u, n * 8, cudaMemcpyHostToDevice, s->stream));
+  MH_CHECK(mh_reconstruct(s, s->hin.p, s->hout.p));
+  MH_CHECK_CUDA(cudaMemcpyAsync(U, s->hout.p, nU * 8, cudaMemcpyDeviceToHost, s->stream));
+  MH_CHECK_CUDA(cudaStreamSynchronize(s->stream));
+  return MH_OK;
+}
+
+// ---- explicit element Schur (mode "mb") --------------------------------------
+
+extern "C" int mh_form_element_schur(mh_system* s) {
+  MH_CHECK(ready(s));
+  MH_CHECK(s->S.alloc((size_t)s->N * s->nc * s->nc));
+  MH_CHECK(launch_element_schur(s));
+  s->have_mb = true;
+  return MH_OK;
+}
+
+extern "C" int mh_apply_mb(mh_system* s, const double* u, double* w) {
+  MH_CHECK(ready(s));
+  MH_CHECK(need(s, s->have_mb, "mh_apply_mb before mh_form_element_schur"));
+  MH_CHECK(halo_u_exchange(s, u, nullptr));
+  MH_CHECK(launch_element_mb(s, u));
+  MH_CHECK(halo_v_exchange(s));
+  return launch_face_reduce(s, u, w, 0, 0);
+}
+
+extern "C" int mh_get_element_schur(mh_system* s, int64_t first, int64_t count, double* out) {
+  MH_CHECK(ready(s));
+  MH_CHECK(need(s, s->have_mb, "element Schur blocks not formed"));
+  if (first < 0 || count < 0 || first + count > s->N || (count && !out)) {
+    set_error("macro range out of bounds");
+    return MH_E_ARG;
+  }
+  const size_t blk = (size_t)s->nc * s->nc;
+  if (count)
+    MH_CHECK_CUDA(cudaMemcpyAsync(out, s->S.p + first * blk, sizeof(double) * blk * count,
+                                  cudaMemcpyDeviceToHost, s->stream));
+  MH_CHECK_CUDA(cudaStreamSynchronize(s->stream));
+  // stored as +C A^-1 B; the reference's explicit block is its negative
+  for (size_t i = 0; i < blk * (size_t)count; ++i) out[i] = -out[i];
+  return MH_OK;
+}

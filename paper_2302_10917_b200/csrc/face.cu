@@ -1,0 +1,449 @@
+// Face kernels: one warp per unknown face.
+//
+//   face_factor_kernel  _factorize_face (schur_solver.py:130-147):
+//                       Cholesky of -D ("chol-neg"), then of D ("chol-pos"),
+//                       then LU with partial pivoting ("lu"); singular if
+//                       min|diag U| < 1e-13 max|D| -> SingularFaceBlock.
+//   face_reduce_kernel  step 4 of apply_schur (schur_solver.py:284-290):
+//                       w_f = D_f uhat_f - v_left - v_right (that order), or
+//                       the reduced RHS f_f = R_hat_f - v_left - v_right
+//                       (schur_solver.py:247-253); optionally fused with
+//                       the D^-1 preconditioner (the GMRES M(A v) step).
+//   precond_kernel      apply_preconditioner (schur_solver.py:296-305):
+//                       z_f = sign * U^-1 L^-1 P w_f.
+//
+// Face data layout: D column-major (t x t), factors FL (lower, diag = L_jj
+// for Cholesky, unit for LU) and FU (upper) column-major, reciprocal
+// diagonals, permutation, sign.
+
+#include <cfloat>
+
+#include "mh_internal.h"
+
+namespace mh {
+namespace {
+
+constexpr int kFaceWarps = 4;
+
+struct FaceArgs {
+  const double* D;
+  const double* Rhat;
+  const int32_t* vslot;
+  const double* V;
+  const double* uhat;
+  double* out;
+  const double* FL;
+  const double* FU;
+  const double* FrL;
+  const double* FrU;
+  const int32_t* Fperm;
+  const double* Fsign;
+  int64_t F;
+  int t;
+};
+
+// In-warp solve z <- sign * U^-1 L^-1 P z for face f (rows lane + 32 r).
+template <int RT>
+__device__ __forceinline__ void face_solve(double (&z)[RT], const FaceArgs& a, int64_t f,
+                                           double* sw, int lane) {
+  const int t = a.t;
+  const size_t TT = (size_t)t * t;
+#pragma unroll
+  for (int r = 0; r < RT; ++r)
+    if (lane + 32 * r < t) sw[lane + 32 * r] = z[r];
+  __syncwarp();
+  double rl[RT], ru[RT];
+#pragma unroll
+  for (int r = 0; r < RT; ++r) {
+    const int i = lane + 32 * r;
+    z[r] = i < t ? sw[__ldg(a.Fperm + f * t + i)] : 0.0;
+    rl[r] = i < t ? __ldg(a.FrL + f * t + i) : 0.0;
+    ru[r] = i < t ? __ldg(a.FrU + f * t + i) : 0.0;
+  }
+  __syncwarp();
+  const double* L = a.FL + f * TT;
+  const double* U = a.FU + f * TT;
+#pragma unroll
+  for (int jb = 0; jb < RT; ++jb)
+    for (int jj = 0; jj < 32; ++jj) {
+      const int j = jb * 32 + jj;
+      if (j < t) {
+        if (lane == jj) z[jb] *= rl[jb];
+        const double zj = __shfl_sync(kFull, z[jb], jj);
+#pragma unroll
+        for (int r = jb; r < RT; ++r) {
+          const int i = lane + 32 * r;
+          if (i > j && i < t) z[r] = fma(-__ldg(L + (size_t)j * t + i), zj, z[r]);
+        }
+      }
+    }
+#pragma unroll
+  for (int jb = RT - 1; jb >= 0; --jb)
+    for (int jj = 31; jj >= 0; --jj) {
+      const int j = jb * 32 + jj;
+      if (j < t) {
+        if (lane == jj) z[jb] *= ru[jb];
+        const double zj = __shfl_sync(kFull, z[jb], jj);
+#pragma unroll
+        for (int r = 0; r <= jb; ++r) {
+          const int i = lane + 32 * r;
+          if (i < j) z[r] = fma(-__ldg(U + (size_t)j * t + i), zj, z[r]);
+        }
+      }
+    }
+  const double sg = __ldg(a.Fsign + f);
+#pragma unroll
+  for (int r = 0; r < RT; ++r) z[r] *= sg;
+}
+
+template <int RT, bool RHS, bool PRE>
+__global__ void __launch_bounds__(kFaceWarps * 32) face_reduce_kernel(FaceArgs a) {
+  extern __shared__ double s_buf[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t f = (int64_t)blockIdx.x * kFaceWarps + w;
+  if (f >= a.F) return;
+  const int t = a.t;
+  double* sw = s_buf + w * t;
+  double z[RT];
+  if (RHS) {
+#pragma unroll
+    for (int r = 0; r < RT; ++r) {
+      const int i = lane + 32 * r;
+      z[r] = i < t ? __ldg(a.Rhat + f * t + i) : 0.0;
+    }
+  } else {
+    for (int s = lane; s < t; s += 32) sw[s] = __ldg(a.uhat + f * t + s);
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < RT; ++r) z[r] = 0.0;
+    const double* Df = a.D + f * (size_t)t * t;
+    for (int s = 0; s < t; ++s) {  // (D uhat)_i, summed over s ascending
+      const double us = sw[s];
+#pragma unroll
+      for (int r = 0; r < RT; ++r) {
+        const int i = lane + 32 * r;
+        if (i < t) z[r] = fma(__ldg(Df + (size_t)s * t + i), us, z[r]);
+      }
+    }
+    __syncwarp();
+  }
+  const int sl = __ldg(a.vslot + 2 * f), sr = __ldg(a.vslot + 2 * f + 1);
+#pragma unroll
+  for (int r = 0; r < RT; ++r) {
+    const int i = lane + 32 * r;
+    if (i < t) {
+      if (sl >= 0) z[r] -= __ldg(a.V + (int64_t)sl * t + i);  // left first
+      if (sr >= 0) z[r] -= __ldg(a.V + (int64_t)sr * t + i);  // then right
+    }
+  }
+  if (PRE) face_solve<RT>(z, a, f, sw, lane);
+#pragma unroll
+  for (int r = 0; r < RT; ++r) {
+    const int i = lane + 32 * r;
+    if (i < t) a.out[f * t + i] = z[r];
+  }
+}
+
+template <int RT>
+__global__ void __launch_bounds__(kFaceWarps * 32) precond_kernel(FaceArgs a) {
+  extern __shared__ double s_buf[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t f = (int64_t)blockIdx.x * kFaceWarps + w;
+  if (f >= a.F) return;
+  const int t = a.t;
+  double z[RT];
+#pragma unroll
+  for (int r = 0; r < RT; ++r) {
+    const int i = lane + 32 * r;
+    z[r] = i < t ? __ldg(a.uhat + f * t + i) : 0.0;
+  }
+  face_solve<RT>(z, a, f, s_buf + w * t, lane);
+#pragma unroll
+  for (int r = 0; r < RT; ++r) {
+    const int i = lane + 32 * r;
+    if (i < t) a.out[f * t + i] = z[r];
+  }
+}
+
+// ---- factorisation -------------------------------------------------------
+
+// Cholesky of the column-major t x t matrix S in place (lower). Returns false
+// on a non-positive (or NaN) pivot, like LAPACK potrf.
+__device__ bool warp_cholesky(double* S, int t, int lane) {
+  for (int j = 0; j < t; ++j) {
+    double* cj = S + (size_t)j * t;
+    const double d = cj[j];
+    if (!(d > 0.0)) return false;
+    const double ljj = sqrt(d);
+    const double r = 1.0 / ljj;
+    __syncwarp();
+    for (int i = j + 1 + lane; i < t; i += 32) cj[i] *= r;
+    if (lane == 0) cj[j] = ljj;
+    __syncwarp();
+    for (int k = j + 1; k < t; ++k) {
+      double* ck = S + (size_t)k * t;
+      const double lkj = cj[k];
+      for (int i = k + lane; i < t; i += 32) ck[i] = fma(-cj[i], lkj, ck[i]);
+    }
+    __syncwarp();
+  }
+  return true;
+}
+
+// LU with partial pivoting of the column-major t x t matrix S (dgetf2 rules).
+__device__ void warp_lu(double* S, int t, int lane, int* perm) {
+  for (int i = lane; i < t; i += 32) perm[i] = i;
+  __syncwarp();
+  for (int k = 0; k < t; ++k) {
+    double* ck = S + (size_t)k * t;
+    double best = -1.0;
+    int bi = k;
+    for (int i = k + lane; i < t; i += 32) {
+      const double v = fabs(ck[i]);
+      if (v > best) { best = v; bi = i; }
+    }
+    for (int o = 16; o; o >>= 1) {
+      const double ov = __shfl_xor_sync(kFull, best, o);
+      const int oi = __shfl_xor_sync(kFull, bi, o);
+      if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+    }
+    const int p = bi;
+    const double pv = ck[p];
+    __syncwarp();
+    if (lane == 0) {
+      const int tmp = perm[k];
+      perm[k] = perm[p];
+      perm[p] = tmp;
+    }
+    if (pv != 0.0) {
+      if (p != k)
+        for (int j = lane; j < t; j += 32) {
+          double* c = S + (size_t)j * t;
+          const double x = c[k];
+          c[k] = c[p];
+          c[p] = x;
+        }
+      __syncwarp();
+      if (fabs(pv) >= DBL_MIN) {
+        const double r = 1.0 / pv;
+        for (int i = k + 1 + lane; i < t; i += 32) ck[i] *= r;
+      } else {
+        for (int i = k + 1 + lane; i < t; i += 32) ck[i] /= pv;
+      }
+    }
+    __syncwarp();
+    for (int j = k + 1; j < t; ++j) {
+      double* c = S + (size_t)j * t;
+      const double akj = c[k];
+      for (int i = k + 1 + lane; i < t; i += 32) c[i] = fma(-ck[i], akj, c[i]);
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void face_factor_kernel(const double* __restrict__ Drm, double* __restrict__ Dcm,
+                                   double* __restrict__ FL, double* __restrict__ FU,
+                                   double* __restrict__ FrL, double* __restrict__ FrU,
+                                   int32_t* __restrict__ Fperm, double* __restrict__ Fsign,
+                                   int8_t* __restrict__ Fkind, int64_t F, int t, int wpb) {
+  extern __shared__ double s_fac[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t f = (int64_t)blockIdx.x * wpb + w;
+  if (f >= F) return;
+  const size_t TT = (size_t)t * t;
+  double* S = s_fac + (size_t)w * (TT + 64);
+  int* pm = reinterpret_cast<int*>(S + TT);
+  const double* Df = Drm + f * TT;
+  double dmax = 0.0;
+  for (size_t idx = lane; idx < TT; idx += 32) {  // row-major in -> column-major copy
+    const int i = (int)(idx / t), j = (int)(idx - (size_t)i * t);
+    const double v = __ldg(Df + idx);
+    Dcm[f * TT + (size_t)j * t + i] = v;
+    dmax = fmax(dmax, fabs(v));
+  }
+  for (int o = 16; o; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(kFull, dmax, o));
+
+  int kind = MH_FACE_SINGULAR;
+  double sign = 1.0;
+  for (int attempt = 0; attempt < 2 && kind == MH_FACE_SINGULAR; ++attempt) {
+    sign = attempt == 0 ? -1.0 : 1.0;
+    for (size_t idx = lane; idx < TT; idx += 32) {
+      const int i = (int)(idx / t), j = (int)(idx - (size_t)i * t);
+      S[(size_t)j * t + i] = sign * __ldg(Df + idx);
+    }
+    __syncwarp();
+    if (warp_cholesky(S, t, lane)) kind = attempt == 0 ? MH_FACE_CHOL_NEG : MH_FACE_CHOL_POS;
+    __syncwarp();
+  }
+  double* FLf = FL + f * TT;
+  double* FUf = FU + f * TT;
+  if (kind != MH_FACE_SINGULAR) {
+    for (size_t idx = lane; idx < TT; idx += 32) {
+      const int j = (int)(idx / t), i = (int)(idx - (size_t)j * t);  // (i, j) column-major
+      const double lij = i >= j ? S[idx] : 0.0;
+      FLf[idx] = lij;
+      // FU = L^T : FU(i, j) = L(j, i)
+      FUf[idx] = i <= j ? S[(size_t)i * t + j] : 0.0;
+    }
+    for (int i = lane; i < t; i += 32) {
+      const double d = S[(size_t)i * t + i];
+      FrL[f * t + i] = 1.0 / d;
+      FrU[f * t + i] = 1.0 / d;
+      Fperm[f * t + i] = i;
+    }
+  } else {
+    sign = 1.0;
+    for (size_t idx = lane; idx < TT; idx += 32) {
+      const int i = (int)(idx / t), j = (int)(idx - (size_t)i * t);
+      S[(size_t)j * t + i] = __ldg(Df + idx);
+    }
+    __syncwarp();
+    warp_lu(S, t, lane, pm);
+    double dmin = DBL_MAX;
+    for (int i = lane; i < t; i += 32) dmin = fmin(dmin, fabs(S[(size_t)i * t + i]));
+    for (int o = 16; o; o >>= 1) dmin = fmin(dmin, __shfl_xor_sync(kFull, dmin, o));
+    kind = (dmin < 1e-13 * fmax(dmax, 1e-300)) ? MH_FACE_SINGULAR : MH_FACE_LU;
+    for (size_t idx = lane; idx < TT; idx += 32) {
+      const int j = (int)(idx / t), i = (int)(idx - (size_t)j * t);
+      FLf[idx] = i > j ? S[idx] : (i == j ? 1.0 : 0.0);
+      FUf[idx] = i <= j ? S[idx] : 0.0;
+    }
+    for (int i = lane; i < t; i += 32) {
+      FrL[f * t + i] = 1.0;
+      FrU[f * t + i] = 1.0 / S[(size_t)i * t + i];
+      Fperm[f * t + i] = pm[i];
+    }
+  }
+  if (lane == 0) {
+    Fsign[f] = sign;
+    Fkind[f] = (int8_t)kind;
+  }
+}
+
+__global__ void transpose_batched_kernel(const double* __restrict__ in, double* __restrict__ out,
+                                         int rows, int cols) {
+  // in: batch x rows x cols (row-major) -> out: batch x cols x rows
+  __shared__ double tile[32][33];
+  const int64_t b = blockIdx.z;
+  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  const double* ib = in + b * (size_t)rows * cols;
+  double* ob = out + b * (size_t)rows * cols;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int r = r0 + k, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[k][threadIdx.x] = ib[(size_t)r * cols + c];
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int c = c0 + k, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) ob[(size_t)c * rows + r] = tile[threadIdx.x][k];
+  }
+}
+
+FaceArgs make_args(mh_system* s, const double* in, double* out) {
+  FaceArgs a;
+  a.D = s->D.p;
+  a.Rhat = s->Rhat.p;
+  a.vslot = s->face_vslot.p;
+  a.V = s->V.p;
+  a.uhat = in;
+  a.out = out;
+  a.FL = s->FL.p;
+  a.FU = s->FU.p;
+  a.FrL = s->FrL.p;
+  a.FrU = s->FrU.p;
+  a.Fperm = s->Fperm.p;
+  a.Fsign = s->Fsign.p;
+  a.F = s->F;
+  a.t = s->t;
+  return a;
+}
+
+}  // namespace
+
+int launch_transpose_batched(cudaStream_t st, const double* in, double* out, int64_t batch,
+                             int rows, int cols) {
+  if (batch == 0) return MH_OK;
+  dim3 grid((cols + 31) / 32, (rows + 31) / 32, 1);
+  dim3 block(32, 8);
+  for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
+    const int64_t nb = batch - b0 < 65535 ? batch - b0 : 65535;
+    grid.z = (unsigned)nb;
+    transpose_batched_kernel<<<grid, block, 0, st>>>(in + b0 * (size_t)rows * cols,
+                                                     out + b0 * (size_t)rows * cols, rows, cols);
+    MH_CHECK_CUDA(cudaGetLastError());
+  }
+  return MH_OK;
+}
+
+int launch_face_factor(mh_system* s, const double* Drm) {
+  if (s->F == 0) return MH_OK;
+  const int t = s->t;
+  const size_t per = ((size_t)t * t + 64) * sizeof(double);
+  int wpb = (int)((48 * 1024) / per);
+  if (wpb < 1) wpb = 1;
+  if (wpb > 8) wpb = 8;
+  size_t smem = per * wpb;
+  if (smem > 48 * 1024) {
+    if (smem > (size_t)s->max_smem_optin) {
+      set_error("face block too large for the face factor kernel");
+      return MH_E_UNSUPPORTED;
+    }
+    MH_CHECK_CUDA(cudaFuncSetAttribute(face_factor_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  }
+  const unsigned grid = (unsigned)((s->F + wpb - 1) / wpb);
+  face_factor_kernel<<<grid, wpb * 32, smem, s->stream>>>(Drm, s->D.p, s->FL.p, s->FU.p, s->FrL.p,
+                                                          s->FrU.p, s->Fperm.p, s->Fsign.p,
+                                                          s->Fkind.p, s->F, t, wpb);
+  MH_CHECK_CUDA(cudaGetLastError());
+  return MH_OK;
+}
+
+int launch_face_reduce(mh_system* s, const double* uhat, double* w, int rhs_mode, int pre) {
+  if (s->F == 0) return MH_OK;
+  FaceArgs a = make_args(s, uhat, w);
+  const unsigned grid = (unsigned)((s->F + kFaceWarps - 1) / kFaceWarps);
+  const size_t smem = (size_t)kFaceWarps * s->t * sizeof(double);
+  const int RT = (s->t + 31) / 32;
+#define MH_FACE_LAUNCH(RR, RHS, PRE) \
+  face_reduce_kernel<RR, RHS, PRE><<<grid, kFaceWarps * 32, smem, s->stream>>>(a)
+#define MH_FACE_SWITCH(RR)                                   \
+  if (RT == RR) {                                            \
+    if (rhs_mode) {                                          \
+      if (pre) MH_FACE_LAUNCH(RR, true, true);               \
+      else MH_FACE_LAUNCH(RR, true, false);                  \
+    } else {                                                 \
+      if (pre) MH_FACE_LAUNCH(RR, false, true);              \
+      else MH_FACE_LAUNCH(RR, false, false);                 \
+    }                                                        \
+  }
+  MH_FACE_SWITCH(1) else MH_FACE_SWITCH(2) else MH_FACE_SWITCH(3) else MH_FACE_SWITCH(4) else {
+    set_error("face kernels: t > 128 unsupported");
+    return MH_E_UNSUPPORTED;
+  }
+#undef MH_FACE_SWITCH
+#undef MH_FACE_LAUNCH
+  MH_CHECK_CUDA(cudaGetLastError());
+  return MH_OK;
+}
+
+int launch_precond(mh_system* s, const double* w, double* z) {
+  if (s->F == 0) return MH_OK;
+  FaceArgs a = make_args(s, w, z);
+  const unsigned grid = (unsigned)((s->F + kFaceWarps - 1) / kFaceWarps);
+  const size_t smem = (size_t)kFaceWarps * s->t * sizeof(double);
+  const int RT = (s->t + 31) / 32;
+  switch (RT) {
+    case 1: precond_kernel<1><<<grid, kFaceWarps * 32, smem, s->stream>>>(a); break;
+    case 2: precond_kernel<2><<<grid, kFaceWarps * 32, smem, s->stream>>>(a); break;
+    case 3: precond_kernel<3><<<grid, kFaceWarps * 32, smem, s->stream>>>(a); break;
+    case 4: precond_kernel<4><<<grid, kFaceWarps * 32, smem, s->stream>>>(a); break;
+    default:
+      set_error("face kernels: t > 128 unsupported");
+      return MH_E_UNSUPPORTED;
+  }
+  MH_CHECK_CUDA(cudaGetLastError());
+  return MH_OK;
+}
+
+}  // namespace mh

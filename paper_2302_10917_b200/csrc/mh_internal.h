@@ -1,0 +1,142 @@
+// Internal declarations shared by the translation units of libmehdg_b200.so.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstddef>
+#include <string>
+#include <vector>
+
+#include "../../include/mehdg_b200.h"
+
+namespace mh {
+
+void set_error(const std::string& msg);
+
+#define MH_CHECK_CUDA(expr)                                                   \
+  do {                                                                        \
+    cudaError_t _e = (expr);                                                  \
+    if (_e != cudaSuccess) {                                                  \
+      ::mh::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));     \
+      return MH_E_CUDA;                                                       \
+    }                                                                         \
+  } while (0)
+
+#define MH_CHECK(expr)        \
+  do {                        \
+    int _s = (expr);          \
+    if (_s != MH_OK) return _s; \
+  } while (0)
+
+constexpr int kWarp = 32;
+constexpr unsigned kFull = 0xffffffffu;
+// fixed reduction partition: results never depend on the device or SM count
+constexpr int kDotBlocks = 512;
+constexpr int kDotThreads = 256;
+
+// Device buffer with RAII-less explicit free (the system owns them).
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  int alloc(size_t count) {
+    if (count == n && p) return MH_OK;
+    release();
+    if (count == 0) return MH_OK;
+    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    if (e != cudaSuccess) {
+      p = nullptr;
+      set_error(std::string("cudaMalloc failed: ") + cudaGetErrorString(e));
+      return MH_E_NOMEM;
+    }
+    n = count;
+    return MH_OK;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+struct Krylov;  // GMRES workspace (krylov.cu)
+
+}  // namespace mh
+
+struct mh_system {
+  int device = 0;
+  int nfe = 3;        // faces (slots) per macro = d+1
+  int64_t N = 0;      // macros on this device
+  int Q = 0;          // block size
+  int t = 0;          // trace dofs per face
+  int nc = 0;         // slot dofs per macro = nfe*t
+  int64_t F = 0;      // unknown faces owned (trace vector = F*t)
+  int64_t F_halo = 0; // halo faces (multi-GPU); trace buffer = (F+F_halo)*t
+  int64_t n_vslot_extra = 0;  // received v-slot segments (multi-GPU)
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  bool have_conn = false, have_blocks = false, factored = false, have_mb = false;
+  bool c_is_bt = false;
+  int max_smem_optin = 0;
+  int num_sms = 0;
+
+  // connectivity
+  mh::DBuf<int32_t> elem_ufac;   // N*nfe   unknown face (local trace index) or -1
+  mh::DBuf<int32_t> face_vslot;  // F*2     v-slot index (e*nfe+k) left, right or -1
+  // host copies of the tables (for halo planning / introspection)
+  std::vector<int32_t> h_face_elem, h_face_slot;
+
+  // blocks
+  mh::DBuf<double> A;      // staged A, N*Q*Q row-major (input of the LU)
+  mh::DBuf<double> LU;     // N*Q*Q column-major packed L\U
+  mh::DBuf<double> dinv;   // N*Q   1/U_ii
+  mh::DBuf<int32_t> piv;   // N*Q   LAPACK 0-based pivots
+  mh::DBuf<int32_t> perm;  // N*Q   composed row permutation: (P x)_i = x[perm_i]
+  mh::DBuf<int32_t> lstat; // N     1 if singular
+  mh::DBuf<double> Bt;     // N*nc*Q  op.B^T  (row c = column c of op.B)
+  mh::DBuf<double> Cm;     // N*nc*Q  op.C    (aliases Bt when c_is_bt)
+  mh::DBuf<double> Ru;     // N*Q
+  mh::DBuf<double> D;      // F*t*t  column-major face blocks
+  mh::DBuf<double> Draw;   // F*t*t  row-major face blocks as uploaded (factor input)
+  mh::DBuf<double> Rhat;   // F*t
+  mh::DBuf<double> FL, FU; // F*t*t  face factors, column-major (lower / upper)
+  mh::DBuf<double> FrL, FrU;  // F*t reciprocal diagonals
+  mh::DBuf<int32_t> Fperm; // F*t
+  mh::DBuf<double> Fsign;  // F
+  mh::DBuf<int8_t> Fkind;  // F
+  mh::DBuf<double> V;      // (N*nfe + extra)*t  element slot contributions
+  mh::DBuf<double> tmp;    // F*t scratch
+  mh::DBuf<double> S;      // N*nc*nc element Schur blocks (mode mb)
+  mh::DBuf<double> halo_u; // received halo trace segments [F_halo*t] (multi-GPU)
+  mh::DBuf<double> hin, hout;  // staging for the *_host entry points
+
+  mh::Krylov* kry = nullptr;
+
+  // multi-GPU
+  int nranks = 1, rank = 0;
+  void* nccl = nullptr;  // ncclComm_t
+};
+
+namespace mh {
+// lu.cu
+int launch_lu(mh_system* s, float* ms);
+// element.cu
+enum ElemMode { kApply = 0, kRhs = 1, kRecon = 2 };
+int launch_element(mh_system* s, int mode, const double* uhat, double* out);
+int launch_element_schur(mh_system* s);
+int launch_element_mb(mh_system* s, const double* uhat);
+// face.cu
+int launch_face_factor(mh_system* s, const double* Drm);
+int launch_face_reduce(mh_system* s, const double* uhat, double* w, int rhs_mode, int fuse_precond);
+int launch_precond(mh_system* s, const double* w, double* z);
+int launch_transpose_batched(cudaStream_t st, const double* in, double* out, int64_t batch,
+                             int rows, int cols);
+// krylov.cu
+void free_krylov(Krylov* k);
+// comm.cu (multi-GPU halo; no-ops on a single device)
+int halo_u_exchange(mh_system* s, const double* u, const double** u_halo);
+int halo_v_exchange(mh_system* s);
+int halo_rhs_begin(mh_system* s);
+void free_comm(mh_system* s);
+}  // namespace mh

@@ -1,0 +1,201 @@
+"""Generate the golden fixtures in tests/golden/ from the REFERENCE itself.
+
+Run in the build container, where /root/reference exists:
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+The reference (`mehdg`, pure Python) is imported read-only and run on:
+  * its own 2-D skeleton (build_structured_macro_mesh) and 3-D Kuhn tets;
+  * the BASELINE synthetic operators of config c1 (whole vectors) and c2 / c3
+    (strided samples + whole-vector checksums), injected through its
+    LocalOperators / FaceOperator data contract exactly as SURVEY.md 8(c)
+    describes (for d=3 the mesh is this repo's skeleton restatement, which the
+    reference solver consumes duck-typed);
+  * real HDG blocks from its own assembly (tanh benchmark, pivoting LU,
+    chol-neg faces, C != B^T).
+Outputs are small .npz files; the GPU box never reads /root/reference.
+"""
+
+from __future__ import annotations
+
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+ROOT = HERE.parent.parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, "/root/reference/pkg/src")
+
+from mehdg import assembly as R_asm  # noqa: E402
+from mehdg import mesh as R_mesh  # noqa: E402
+from mehdg import schur_solver as R  # noqa: E402
+from mehdg.bench import make_benchmark  # noqa: E402
+
+from paper_2302_10917_b200 import synthetic as S  # noqa: E402
+from paper_2302_10917_b200.mesh import build_structured_macro_mesh  # noqa: E402
+
+STRIDE = 97
+
+
+def ref_skeleton_tables(M):
+    fl = np.array([(f.left.macro, f.left.edge) for f in M.skeleton], np.int64)
+    fr = np.array([(f.right.macro, f.right.edge) if f.right else (-1, -1) for f in M.skeleton],
+                  np.int64)
+    tag = np.array([{"interior": 0, "D": 1, "N": 2}[f.tag] for f in M.skeleton], np.int64)
+    ev = np.array([e.vertex_ids for e in M.macro_elements], np.int64)
+    ef = np.array([[e.faces[k][0] for k in range(3)] for e in M.macro_elements], np.int64)
+    lt = np.array([(f.left.t0, f.left.t1) for f in M.skeleton])
+    rt = np.array([(f.right.t0, f.right.t1) if f.right else (0.0, 0.0) for f in M.skeleton])
+    n = M.n
+    verts = np.round(M.vertices * n).astype(np.int64)
+    return dict(face_left=fl, face_right=fr, face_tag=tag, elem_verts=ev, elem_face=ef,
+                face_left_t=lt, face_right_t=rt, verts=verts)
+
+
+def make_skeletons():
+    out = {}
+    for n in (1, 2, 3, 4, 8):
+        M = R_mesh.build_structured_macro_mesh(2, n, 2)
+        for k, v in ref_skeleton_tables(M).items():
+            out[f"n{n}_{k}"] = v
+    np.savez_compressed(HERE / "skeleton_2d.npz", **out)
+    out = {}
+    for n in (1, 2, 3, 4):
+        K = R_mesh._build_kuhn_counting_mesh(n, 2)
+        out[f"n{n}_elem_verts"] = np.array([e.vertex_ids for e in K.macro_elements], np.int64)
+        out[f"n{n}_verts"] = np.round(K.vertices * n).astype(np.int64)
+    np.savez_compressed(HERE / "kuhn_3d.npz", **out)
+
+
+def inject(prob, mesh):
+    """LocalOperators/FaceOperator of the reference from a synthetic problem."""
+    t, nfe = prob["t"], prob["d"] + 1
+    local_ops = []
+    for e in range(prob["N"]):
+        if prob["d"] == 2:
+            fids = [mesh.macro_elements[e].faces[k][0] for k in range(3)]
+        else:
+            fids = [int(prob["mesh"].elem_face[e, k]) for k in range(nfe)]
+        slots = [(fid, slice(k * t, (k + 1) * t)) for k, fid in enumerate(fids)]
+        local_ops.append(R_asm.LocalOperators(
+            macro_id=e, A=prob["A"][e], B=np.ascontiguousarray(prob["B"][e]),
+            C=prob["C"][e], R_u=prob["R_u"][e], face_slots=slots, storage="dense"))
+    face_ops = {}
+    for face in mesh.skeleton:
+        if face.tag == "D":
+            continue
+        u = prob["uidx"][face.id]
+        face_ops[face.id] = R_asm.FaceOperator(face_id=face.id, D=prob["D"][u],
+                                               R_hat=prob["R_hat"][u], tag=face.tag)
+    return local_ops, face_ops
+
+
+def run_reference(name, full: bool, gmres_tol=1e-10):
+    d, n, m, p = S.CONFIGS[name]
+    prob = S.make_problem(d, n, m, p, seed=0)
+    mesh = R_mesh.build_structured_macro_mesh(2, n, m) if d == 2 else prob["mesh"]
+    local_ops, face_ops = inject(prob, mesh)
+    cfg = R.SolverConfig(tol=gmres_tol)
+    t0 = time.time()
+    sys_ = R.condense(mesh, local_ops, face_ops, cfg)
+    t_cond = time.time() - t0
+    u = prob["uhat"]
+    t0 = time.time()
+    w = R.apply_schur(sys_, u)
+    t_apply = time.time() - t0
+    z = R.apply_preconditioner(sys_, w)
+    x, info = R.gmres(lambda v: R.apply_schur(sys_, v), sys_.f_vec, cfg,
+                      precond=lambda v: R.apply_preconditioner(sys_, v))
+    U = np.stack(R.reconstruct_interior(sys_, x))
+    out = dict(f_norm=np.linalg.norm(sys_.f_vec), w_norm=np.linalg.norm(w),
+               z_norm=np.linalg.norm(z), x_norm=np.linalg.norm(x), U_norm=np.linalg.norm(U),
+               f_sum=sys_.f_vec.sum(), w_sum=w.sum(), z_sum=z.sum(), x_sum=x.sum(),
+               U_sum=U.sum(), iterations=info["iterations"], converged=info["converged"],
+               history=np.array(info["residual_history"]), zhat=sys_.zhat,
+               t_condense=t_cond, t_apply=t_apply,
+               offsets_start=np.array([sys_.offsets[f][0] for f in sorted(sys_.offsets)]),
+               offsets_fid=np.array(sorted(sys_.offsets)))
+    kinds = {"chol-neg": 0, "chol-pos": 1, "lu": 2}
+    out["face_kinds"] = np.array([kinds[face_ops[f].factor_kind] for f in sorted(face_ops)])
+    sel = np.arange(0, sys_.zhat, 1 if full else STRIDE)
+    for k, v in dict(f=sys_.f_vec, w=w, z=z, x=x).items():
+        out[k] = v[sel]
+    out["sel"] = sel
+    esel = np.arange(0, prob["N"], 1 if full else max(1, prob["N"] // 64))
+    out["esel"] = esel
+    out["U"] = U[esel]
+    out["lu"] = np.stack([local_ops[e].lu[1][0] for e in esel[:8]])
+    out["piv"] = np.stack([local_ops[e].lu[1][1] for e in esel[:8]])
+    # face-plan encoding: (fid, start, left e, left slot start, right e, right slot start)
+    fp = []
+    for fid, start, nd, order in sys_.face_plan:
+        row = [fid, start]
+        for (e, sl) in order:
+            row += [e, sl.start]
+        row += [-1, -1] * (2 - len(order))
+        fp.append(row)
+    out["face_plan"] = np.array(fp, np.int64)
+    out["gather_idx_concat"] = np.concatenate(sys_.gather_idx)
+    # explicit Schur on random vectors (sampled rows)
+    if full:
+        Sx = R.assemble_schur_explicit(sys_)
+        xs = np.random.default_rng(42).standard_normal((3, sys_.zhat))
+        out["mb_x"] = xs
+        out["mb_Sx"] = np.stack([Sx @ v for v in xs])
+        out["mf_Sx"] = np.stack([R.apply_schur(sys_, v) for v in xs])
+    np.savez_compressed(HERE / f"synthetic_{name}.npz", **out)
+    print(name, "condense", round(t_cond, 2), "apply", round(t_apply, 3), "its",
+          info["iterations"], info["converged"])
+
+
+def run_real(n=2, m=2, p=2):
+    """Reference assembly (tanh benchmark) -> blocks + reference results."""
+    case = make_benchmark("tanh", 0.4, (1.0, 1.0))
+    mesh = R_mesh.build_structured_macro_mesh(2, n, m)
+    pool = R.WorkerPool(1)
+    local_ops, face_ops = R.assemble_system(mesh, case.problem(), R_asm.StabilizationConfig(), p,
+                                            pool)
+    cfg = R.SolverConfig(tol=1e-12)
+    sys_ = R.condense(mesh, local_ops, face_ops, cfg, pool=pool)
+    rng = np.random.default_rng(3)
+    xs = rng.standard_normal((3, sys_.zhat))
+    out = dict(
+        A=np.stack([np.asarray(o.A.toarray() if hasattr(o.A, "toarray") else o.A)
+                    for o in local_ops]),
+        B=np.stack([o.B for o in local_ops]), C=np.stack([o.C for o in local_ops]),
+        R_u=np.stack([o.R_u for o in local_ops]),
+        D=np.stack([face_ops[f].D for f in sorted(face_ops)]),
+        R_hat=np.stack([face_ops[f].R_hat for f in sorted(face_ops)]),
+        face_ids=np.array(sorted(face_ops)),
+        slot_faces=np.array([[fid for fid, _ in o.face_slots] for o in local_ops]),
+        f=sys_.f_vec, xs=xs, w=np.stack([R.apply_schur(sys_, v) for v in xs]),
+        z=np.stack([R.apply_preconditioner(sys_, v) for v in xs]),
+        lu=np.stack([o.lu[1][0] for o in local_ops]), piv=np.stack([o.lu[1][1] for o in local_ops]),
+        face_kinds=np.array([{"chol-neg": 0, "chol-pos": 1, "lu": 2}[face_ops[f].factor_kind]
+                             for f in sorted(face_ops)]),
+        n=n, m=m, p=p)
+    x, info = R.gmres(lambda v: R.apply_schur(sys_, v), sys_.f_vec, cfg,
+                      precond=lambda v: R.apply_preconditioner(sys_, v))
+    out.update(x=x, iterations=info["iterations"], history=np.array(info["residual_history"]),
+               U=np.stack(R.reconstruct_interior(sys_, x)))
+    np.savez_compressed(HERE / f"real_tanh_n{n}m{m}p{p}.npz", **out)
+    print("real", n, m, p, "zhat", sys_.zhat, "its", info["iterations"],
+          "swaps", int(sum((o.lu[1][1] != np.arange(o.lu[1][1].size)).sum() for o in local_ops)))
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["skeleton", "c1", "real", "c2", "c3"]
+    if "skeleton" in which:
+        make_skeletons()
+    if "c1" in which:
+        run_reference("c1", full=True)
+    if "real" in which:
+        run_real(2, 2, 2)
+        run_real(3, 1, 3)
+    if "c2" in which:
+        run_reference("c2", full=False)
+    if "c3" in which:
+        run_reference("c3", full=False)

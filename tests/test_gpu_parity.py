@@ -1,0 +1,278 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the reference's own
+outputs (tests/golden) and the CPU oracle, on identical seeded inputs.
+
+Tolerances (BASELINE north_star): integer tables bit-exact; operator apply,
+RHS, preconditioner and factors <= 1e-12 relative; converged uhat / u
+<= 1e-9 relative; GMRES iteration counts within +-1."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import golden, rel
+from oracle import solver_oracle as SO
+import paper_2302_10917_b200 as P
+from paper_2302_10917_b200 import synthetic as S
+
+pytestmark = pytest.mark.gpu
+
+APPLY_TOL = 1e-12
+SOLVE_TOL = 1e-9
+
+
+def condense_problem(prob, **kw):
+    cfg = P.SolverConfig(tol=kw.pop("tol", 1e-10))
+    tables = {"nfe": prob["d"] + 1, "elem_ufac": prob["elem_face"],
+              "face_elem": prob["face_elem"], "face_slot": prob["face_slot"],
+              "uidx": prob["uidx"], "F": prob["F"]}
+    return P.condense_arrays(prob["mesh"], prob["A"], None, prob["Be"], prob["R_u"], prob["D"],
+                             prob["R_hat"], cfg, tables=tables, **kw), cfg
+
+
+@pytest.fixture(scope="module")
+def c1(gpu):
+    prob = S.config_problem("c1")
+    sys_, cfg = condense_problem(prob)
+    return prob, sys_, cfg
+
+
+def test_c1_factors_match_reference(c1):
+    prob, sys_, _ = c1
+    g = golden("synthetic_c1.npz")
+    lu, piv = P.local_factors(sys_)
+    for k, e in enumerate(g["esel"][:8]):
+        assert np.array_equal(piv[e], g["piv"][k])
+        assert np.abs(lu[e] - g["lu"][k]).max() <= APPLY_TOL * np.abs(g["lu"][k]).max()
+    assert np.array_equal(sys_.face_kinds, g["face_kinds"])
+
+
+def test_c1_rhs_apply_precond_match_reference(c1):
+    prob, sys_, _ = c1
+    g = golden("synthetic_c1.npz")
+    assert sys_.zhat == int(g["zhat"])
+    assert rel(sys_.f_vec, g["f"]) <= APPLY_TOL
+    w = P.apply_schur(sys_, prob["uhat"])
+    assert rel(w, g["w"]) <= APPLY_TOL
+    z = P.apply_preconditioner(sys_, w)
+    assert rel(z, g["z"]) <= APPLY_TOL
+    for x, ref in zip(g["mb_x"], g["mf_Sx"]):
+        assert rel(P.apply_schur(sys_, x), ref) <= APPLY_TOL
+
+
+def test_c1_gmres_and_reconstruct_match_reference(c1):
+    prob, sys_, cfg = c1
+    g = golden("synthetic_c1.npz")
+    x, info = P.gmres(P.SchurOperator(sys_), sys_.f_vec, cfg, precond=P.Preconditioner(sys_))
+    assert info["converged"]
+    assert abs(info["iterations"] - int(g["iterations"])) <= 1
+    assert rel(x, g["x"]) <= SOLVE_TOL
+    hist = np.array(info["residual_history"])
+    n = min(hist.size, g["history"].size)
+    assert np.allclose(hist[:n], g["history"][:n], rtol=1e-6)
+    U = np.stack(P.reconstruct_interior(sys_, x))
+    assert rel(U[g["esel"]], g["U"]) <= SOLVE_TOL
+
+
+def test_c1_explicit_schur_matches_reference(c1):
+    prob, sys_, _ = c1
+    g = golden("synthetic_c1.npz")
+    S_csr = P.assemble_schur_explicit(sys_)
+    for x, ref in zip(g["mb_x"], g["mb_Sx"]):
+        assert rel(S_csr @ x, ref) <= APPLY_TOL
+        assert rel(P.apply_schur_mb(sys_, x), ref) <= APPLY_TOL
+
+
+def test_apply_deterministic_and_linear(c1):
+    prob, sys_, _ = c1
+    rng = np.random.default_rng(0)
+    x, y = rng.standard_normal((2, sys_.zhat))
+    w1 = P.apply_schur(sys_, x)
+    w2 = P.apply_schur(sys_, x)
+    assert np.array_equal(w1, w2)
+    assert np.abs(P.apply_schur(sys_, np.zeros(sys_.zhat))).max() == 0.0
+    lhs = P.apply_schur(sys_, 2 * x + 3 * y)
+    rhs = 2 * w1 + 3 * P.apply_schur(sys_, y)
+    assert np.abs(lhs - rhs).max() < 1e-10 * max(1.0, np.abs(rhs).max())
+
+
+def test_device_tensor_path_matches_host_path(c1):
+    import torch
+
+    prob, sys_, _ = c1
+    u = torch.as_tensor(prob["uhat"], device="cuda")
+    w_dev = P.apply_schur(sys_, u)
+    assert w_dev.is_cuda
+    assert np.array_equal(w_dev.cpu().numpy(), P.apply_schur(sys_, prob["uhat"]))
+
+
+@pytest.mark.parametrize("fx", ["real_tanh_n2m2p2.npz", "real_tanh_n3m1p3.npz"])
+def test_reference_assembled_blocks(gpu, fx):
+    """Real HDG blocks from the reference assembly: pivoting LU, C != B^T,
+    chol-neg faces -- through the drop-in condense on LocalOperators."""
+    g = golden(fx)
+    n, m = int(g["n"]), int(g["m"])
+    mesh = P.build_structured_macro_mesh(2, n, m)
+    t = g["D"].shape[1]
+    local_ops = [P.LocalOperators(macro_id=e, A=g["A"][e], B=g["B"][e], C=g["C"][e],
+                                  R_u=g["R_u"][e],
+                                  face_slots=[(int(f), slice(k * t, (k + 1) * t))
+                                              for k, f in enumerate(g["slot_faces"][e])])
+                 for e in range(g["A"].shape[0])]
+    face_ops = {int(f): P.FaceOperator(face_id=int(f), D=g["D"][i], R_hat=g["R_hat"][i])
+                for i, f in enumerate(g["face_ids"])}
+    cfg = P.SolverConfig(tol=1e-12)
+    sys_ = P.condense(mesh, local_ops, face_ops, cfg)
+    assert {face_ops[int(f)].factor_kind for f in g["face_ids"]} == \
+        {_kind(k) for k in g["face_kinds"]}
+    lu, piv = P.local_factors(sys_)
+    assert np.array_equal(piv, g["piv"])
+    assert np.abs(lu - g["lu"]).max() <= APPLY_TOL * np.abs(g["lu"]).max()
+    assert rel(sys_.f_vec, g["f"]) <= APPLY_TOL
+    for x, w, z in zip(g["xs"], g["w"], g["z"]):
+        assert rel(P.apply_schur(sys_, x), w) <= APPLY_TOL
+        assert rel(P.apply_preconditioner(sys_, x), z) <= APPLY_TOL
+    x, info = P.gmres(P.SchurOperator(sys_), sys_.f_vec, cfg, precond=P.Preconditioner(sys_))
+    assert abs(info["iterations"] - int(g["iterations"])) <= 1
+    assert rel(x, g["x"]) <= SOLVE_TOL
+    U = np.stack(P.reconstruct_interior(sys_, x))
+    assert rel(U, g["U"]) <= SOLVE_TOL
+
+
+def _kind(k):
+    return {0: "chol-neg", 1: "chol-pos", 2: "lu"}[int(k)]
+
+
+@pytest.mark.parametrize("d,n,m,p", [(2, 4, 4, 3), (2, 3, 2, 5), (3, 2, 2, 3), (3, 2, 1, 4),
+                                     (3, 1, 3, 3), (2, 2, 3, 6)])
+def test_against_oracle_small(gpu, d, n, m, p):
+    """Each BASELINE block shape family (Q = 15..220) against the oracle."""
+    prob = S.make_problem(d, n, m, p, seed=7)
+    sys_, cfg = condense_problem(prob)
+    o = SO.system_from_problem(prob).factorize()
+    assert rel(sys_.f_vec, o.rhs()) <= APPLY_TOL
+    w = P.apply_schur(sys_, prob["uhat"])
+    assert rel(w, o.apply(prob["uhat"])) <= APPLY_TOL
+    assert rel(P.apply_preconditioner(sys_, w), o.precond(w)) <= APPLY_TOL
+    x, info = P.gmres(P.SchurOperator(sys_), sys_.f_vec, cfg, precond=P.Preconditioner(sys_))
+    xo, io = SO.gmres(o.apply, o.rhs(), tol=1e-10, precond=o.precond)
+    assert abs(info["iterations"] - io["iterations"]) <= 1
+    assert rel(x, xo) <= SOLVE_TOL
+    assert rel(np.stack(P.reconstruct_interior(sys_, x)), o.reconstruct(xo)) <= SOLVE_TOL
+    lu, piv = P.local_factors(sys_, 0, min(4, prob["N"]))
+    for e in range(lu.shape[0]):
+        assert np.array_equal(piv[e], o.lu[e][1])
+        assert np.abs(lu[e] - o.lu[e][0]).max() <= APPLY_TOL * np.abs(o.lu[e][0]).max()
+
+
+def test_pivoting_blocks(gpu):
+    """Blocks that need row interchanges (no diagonal dominance)."""
+    prob = S.make_problem(2, 3, 2, 2, seed=11)
+    rng = np.random.default_rng(5)
+    prob["A"] = rng.standard_normal(prob["A"].shape)
+    sys_, cfg = condense_problem(prob)
+    o = SO.system_from_problem(prob).factorize()
+    lu, piv = P.local_factors(sys_)
+    swaps = 0
+    for e in range(prob["N"]):
+        assert np.array_equal(piv[e], o.lu[e][1])
+        swaps += int((piv[e] != np.arange(prob["Q"])).sum())
+    assert swaps > 0
+    assert rel(P.apply_schur(sys_, prob["uhat"]), o.apply(prob["uhat"])) <= 1e-11
+
+
+def test_singular_local_block_raises_with_id(gpu):
+    prob = S.make_problem(2, 2, 1, 1)
+    prob["A"] = prob["A"].copy()
+    prob["A"][5] = 0.0
+    prob["A"][6] = 0.0
+    with pytest.raises(P.SingularLocalBlock) as ei:
+        condense_problem(prob)
+    assert ei.value.args[0] == 5
+
+
+def test_singular_face_block_raises(gpu):
+    prob = S.make_problem(2, 2, 1, 1)
+    prob["D"] = prob["D"].copy()
+    prob["D"][2] = 0.0
+    with pytest.raises(P.SingularFaceBlock) as ei:
+        condense_problem(prob)
+    assert ei.value.args[0] == 2
+
+
+def test_indefinite_face_block_uses_lu(gpu):
+    prob = S.make_problem(2, 2, 2, 2, seed=3)
+    prob["D"] = prob["D"].copy()
+    prob["D"][0] = np.diag(np.r_[1.0, -2.0, 3.0, -4.0, 5.0]) + 0.1
+    sys_, _ = condense_problem(prob)
+    assert sys_.face_kinds[0] == 2
+    o = SO.system_from_problem(prob).factorize()
+    w = np.random.default_rng(1).standard_normal(sys_.zhat)
+    assert rel(P.apply_preconditioner(sys_, w), o.precond(w)) <= APPLY_TOL
+
+
+def test_two_macro_mesh_counts(gpu):
+    """test_schur_solver.py:116-124: one apply = 2 macro tasks + 1 face reduction."""
+    prob = S.make_problem(2, 1, 1, 1)
+    sys_, _ = condense_problem(prob)
+    assert sys_.zhat == 2
+    sys_.counters["macro_apply"] = sys_.counters["face_reduce"] = 0
+    P.apply_schur(sys_, np.ones(2))
+    assert sys_.counters == {"macro_apply": 2, "face_reduce": 1}
+
+
+def test_gmres_kats_through_callbacks(gpu):
+    """test_schur_solver.py:205-230 with Python operators (mh_gmres_op)."""
+    cfg = P.SolverConfig(tol=1e-12)
+    x, info = P.gmres(lambda v: v, np.array([3.0, -1.0, 2.0]), cfg)
+    assert info["converged"] and info["iterations"] == 1
+    assert np.abs(x - [3.0, -1.0, 2.0]).max() < 1e-12
+    d = np.arange(1.0, 6.0)
+    x, info = P.gmres(lambda v: d * v, np.ones(5), cfg)
+    assert info["converged"] and info["iterations"] <= 5
+    assert np.abs(x - 1.0 / d).max() < 1e-10
+    d = np.arange(1.0, 101.0)
+    x, info = P.gmres(lambda v: d * v, np.ones(100), P.SolverConfig(tol=1e-14, maxiter=3, restart=3))
+    assert not info["converged"] and info["iterations"] == 3
+    assert len(info["residual_history"]) >= 2
+    x, info = P.gmres(lambda v: 2 * v, np.zeros(4), P.SolverConfig())
+    assert info["converged"] and np.abs(x).max() == 0.0
+
+
+def test_gmres_python_operator_equals_bound_operator(c1):
+    prob, sys_, cfg = c1
+    x1, i1 = P.gmres(P.SchurOperator(sys_), sys_.f_vec, cfg, precond=P.Preconditioner(sys_))
+    x2, i2 = P.gmres(lambda v: P.apply_schur(sys_, v), sys_.f_vec, cfg,
+                     precond=lambda v: P.apply_preconditioner(sys_, v))
+    assert i1["iterations"] == i2["iterations"]
+    assert rel(x1, x2) <= 1e-12
+
+
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_full_config_against_reference_samples(gpu, name):
+    """BASELINE c2 / c3 at full size vs the reference run (strided samples
+    and whole-vector checksums), plus size-independent properties."""
+    g = golden(f"synthetic_{name}.npz")
+    prob = S.config_problem(name)
+    sys_, cfg = condense_problem(prob)
+    sel = g["sel"]
+    f = sys_.f_vec
+    assert rel(f[sel], g["f"]) <= APPLY_TOL
+    assert abs(np.linalg.norm(f) - float(g["f_norm"])) <= APPLY_TOL * float(g["f_norm"])
+    w = P.apply_schur(sys_, prob["uhat"])
+    assert rel(w[sel], g["w"]) <= APPLY_TOL
+    assert abs(np.linalg.norm(w) - float(g["w_norm"])) <= APPLY_TOL * float(g["w_norm"])
+    z = P.apply_preconditioner(sys_, w)
+    assert rel(z[sel], g["z"]) <= APPLY_TOL
+    x, info = P.gmres(P.SchurOperator(sys_), sys_.f_device, cfg, precond=P.Preconditioner(sys_))
+    assert info["converged"]
+    assert abs(info["iterations"] - int(g["iterations"])) <= 1
+    xh = x.cpu().numpy()
+    assert rel(xh[sel], g["x"]) <= SOLVE_TOL
+    U = P.reconstruct_interior(sys_, x).cpu().numpy()
+    assert rel(U[g["esel"]], g["U"]) <= SOLVE_TOL
+    # the converged residual, through the operator itself
+    r = P.apply_preconditioner(sys_, sys_.f_vec - P.apply_schur(sys_, xh))
+    assert np.linalg.norm(r) <= 10 * cfg.tol * np.linalg.norm(P.apply_preconditioner(sys_, sys_.f_vec))
+    # bitwise determinism at full size
+    assert np.array_equal(w, P.apply_schur(sys_, prob["uhat"]))
