@@ -1,0 +1,425 @@
+"""Benchmark of the B200 Schur-operator path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+One *step* is one matrix-free Schur-operator apply w = (D - C A^-1 B) uhat over
+every macro and unknown face of the workload (BASELINE configs[1] = c2 on one
+GPU: d=2, n=128, m=4, p=3, N=32768 macros, Q=91, t=13, zhat=635,648), with the
+seeded synthetic blocks of paper_2302_10917_b200.synthetic resident in HBM.
+The blocks (3.2 GB per apply) are far larger than the 126 MB L2, so no L2
+flush is needed between steps.
+
+Prints ONE JSON line (rank 0):  value = applies/s of the whole job (device
+time, CUDA events on the library's stream, max over ranks), plus
+  roofline      the element kernel (dominant) vs the measured HBM copy peak
+  e2e           the same metric through the public API with pinned host buffers
+                (H2D of uhat and D2H of w inside every step)
+  lu            batched LU GFLOP/s (fp64) of the factorisation kernel
+  solve         GMRES(100) + D^-1 to 1e-10: iterations and seconds
+  cpu_baseline  the CPU oracle (restatement of the reference algorithm) timed
+                on a bounded sample of the same workload on this host.
+`--impl reference` times that CPU restatement alone (the reference is pure
+Python and cannot be installed on the GPU box).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+BASELINE_METRIC = "Schur-operator applies/sec & HBM GB/s (% roofline); batched LU GFLOP/s fp64"
+UNIT = "applies/s"
+
+
+def measured_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+        self.active = False
+        self._thr = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "20"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self._thr = threading.Thread(target=self._read, daemon=True)
+        self._thr.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            if self.active:
+                self.samples.append(line.strip())
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], 0.0, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for s in self.samples:
+            parts = [x.strip() for x in s.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for name, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle leg (bounded sample of the same workload)
+
+def oracle_sample(prob: dict, n_macros: int, threads: int = 1):
+    """An OracleSystem over macros [0, n_macros) of the workload and the unknown
+    faces whose left side lies in it (right sides outside are dropped)."""
+    from oracle import solver_oracle as SO
+
+    ns = min(n_macros, prob["N"])
+    fe, fs = prob["face_elem"], prob["face_slot"]
+    keep = fe[:, 0] < ns
+    fidx = np.nonzero(keep)[0]
+    remap = -np.ones(prob["F"], np.int64)
+    remap[fidx] = np.arange(fidx.size)
+    ef = prob["elem_face"][:ns].astype(np.int64)
+    ef = np.where(ef >= 0, remap[np.maximum(ef, 0)], -1)
+    fe_s = fe[fidx].astype(np.int64).copy()
+    fs_s = fs[fidx].astype(np.int64).copy()
+    outside = fe_s[:, 1] >= ns
+    fe_s[outside, 1] = -1
+    fs_s[outside, 1] = -1
+    o = SO.OracleSystem(prob["A"][:ns], prob["B"][:ns], prob["C"][:ns], prob["R_u"][:ns],
+                        prob["D"][fidx], prob["R_hat"][fidx], ef, fe_s, fs_s, prob["t"])
+    return o, ns, int(fidx.size)
+
+
+def time_oracle(prob: dict, n_macros: int, reps: int, threads: int):
+    """Oracle factorisation + `reps` applies on the sample; returns a dict."""
+    from threadpoolctl import threadpool_limits
+
+    with threadpool_limits(limits=threads):
+        o, ns, fs = oracle_sample(prob, n_macros)
+        t0 = time.perf_counter()
+        o.factorize()
+        t_fac = time.perf_counter() - t0
+        u = np.random.default_rng(1).standard_normal(o.zhat)
+        o.apply(u)
+        times = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            o.apply(u)
+            times.append(time.perf_counter() - t0)
+    scale = prob["N"] / ns
+    t_apply = float(np.mean(times)) * scale
+    lu_gflops = (2.0 / 3.0) * prob["Q"] ** 3 * ns / t_fac / 1e9
+    return {"apply_s_full": t_apply, "applies_per_s": 1.0 / t_apply, "sample_macros": ns,
+            "sample_faces": fs, "scale": scale, "lu_gflops": lu_gflops, "reps": reps,
+            "sample_apply_s": float(np.mean(times))}
+
+
+# ---------------------------------------------------------------------------
+
+def config_block(name, prob, world):
+    return {"workload": f"BASELINE {name}: d={prob['d']} n={prob['n']} m={prob['m']} "
+                        f"p={prob['p']} fp64 seed={prob['seed']}",
+            "N_macros": prob["N"], "Q": prob["Q"], "t": prob["t"], "nc": prob["nc"],
+            "F_unknown": prob["F"], "zhat": prob["zhat"],
+            "operator": "matrix-free D - C A^-1 B (C = B^T synthetic, B_e streamed once)",
+            "l2_flush": "none needed: 3.2 GB of blocks per apply >> 126 MB L2",
+            "parallelism": f"replicas{world}" if world > 1 else "single"}
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the CPU restatement of the reference algorithm."""
+    if rank != 0:
+        return 0
+    from paper_2302_10917_b200 import synthetic as S
+
+    d, n, m, p = S.CONFIGS[args.config]
+    prob = S.make_problem(d, n, m, p, seed=args.seed)
+    threads = os.cpu_count() or 1
+    ns = args.cpu_sample
+    from threadpoolctl import threadpool_limits
+    import concurrent.futures as cf
+
+    with threadpool_limits(limits=threads):
+        o, ns, fs = oracle_sample(prob, ns)
+        o.factorize()
+        u = np.random.default_rng(1).standard_normal(o.zhat)
+        for _ in range(args.warmup):
+            o.apply(u)
+        times = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            o.apply(u)
+            times.append(time.perf_counter() - t0)
+    scale = prob["N"] / ns
+    ms = float(np.mean(times)) * scale * 1e3
+    value = 1e3 / ms
+    sample = (f"oracle port (per-macro scipy LAPACK loop as schur_solver.apply_schur) on macros "
+              f"[0,{ns}) of {prob['N']} and their {fs} faces; per-step time x{scale:.1f}")
+    line = {"impl": "reference", "metric": BASELINE_METRIC, "value": value, "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded BASELINE generator)",
+            "config": config_block(args.config, prob, 1),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def run_ours(args, world, rank, local):
+    import ctypes as C
+
+    import torch
+
+    import paper_2302_10917_b200 as P
+    from paper_2302_10917_b200 import _lib, synthetic as S
+    from paper_2302_10917_b200._lib import check, lib, ptr
+
+    dev = local
+    torch.cuda.set_device(dev)
+    d, n, m, p = S.CONFIGS[args.config]
+    t0 = time.perf_counter()
+    prob = S.make_problem(d, n, m, p, seed=args.seed)
+    t_gen = time.perf_counter() - t0
+    tables = {"nfe": d + 1, "elem_ufac": prob["elem_face"], "face_elem": prob["face_elem"],
+              "face_slot": prob["face_slot"], "uidx": prob["uidx"], "F": prob["F"]}
+    cfg = P.SolverConfig(tol=1e-10, device=dev)
+    t0 = time.perf_counter()
+    sys_ = P.condense_arrays(prob["mesh"], prob["A"], None, prob["Be"], prob["R_u"], prob["D"],
+                             prob["R_hat"], cfg, tables=tables, device=dev)
+    t_condense = time.perf_counter() - t0
+    h = sys_.handle
+    stream = torch.cuda.current_stream(dev)
+    N, Q, nc, t, F = prob["N"], prob["Q"], prob["nc"], prob["t"], prob["F"]
+
+    # ---- batched LU ----------------------------------------------------------
+    lu_ms = []
+    for i in range(4):
+        ms = C.c_float()
+        check(lib.mh_refactorize_local(h, C.byref(ms)), "lu")
+        if i:
+            lu_ms.append(ms.value)
+    lu_ms = float(np.mean(lu_ms))
+    lu_flops = S.lu_flops(N, Q)
+
+    # ---- device-resident applies --------------------------------------------
+    u = torch.as_tensor(prob["uhat"], device=f"cuda:{dev}")
+    w = torch.empty_like(u)
+    for _ in range(args.warmup):
+        check(lib.mh_apply(h, ptr(u), ptr(w)), "apply")
+    sampler = ClockSampler(dev)
+    sampler.start()
+    time.sleep(0.3)
+    barrier(world)
+    torch.cuda.synchronize(dev)
+    check(lib.mh_profile(h, 1), "profile")
+    check(lib.mh_profile_read(h, None, None, None, None), "profile")
+    sampler.active = True
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        check(lib.mh_apply(h, ptr(u), ptr(w)), "apply")
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    sampler.active = False
+    barrier(world)
+    elapsed_ms = e0.elapsed_time(e1)
+    el_ms, el_n, fa_ms, fa_n = C.c_double(), C.c_int64(), C.c_double(), C.c_int64()
+    check(lib.mh_profile_read(h, C.byref(el_ms), C.byref(el_n), C.byref(fa_ms), C.byref(fa_n)),
+          "profile")
+    check(lib.mh_profile(h, 0), "profile")
+    sampler.stop()
+    elapsed_ms = max_over_ranks(elapsed_ms, world)
+    ms_per_step = elapsed_ms / args.steps
+    value = world * 1e3 / ms_per_step
+
+    bytes_apply = S.algorithmic_bytes_per_apply(N, Q, nc, d, F, t)
+    elem_bytes = N * (8 * Q * Q + 4 * Q + 8 * nc * Q + 16 * nc + 4 * (d + 1))
+    elem_avg_ms = el_ms.value / max(el_n.value, 1)
+    face_avg_ms = fa_ms.value / max(fa_n.value, 1)
+    peaks = measured_peaks()
+    achieved = elem_bytes / (elem_avg_ms * 1e-3) / 1e9
+    traffic = None
+    prof_json = ROOT / "profiles" / f"ncu_traffic_{args.config}.json"
+    if prof_json.exists():
+        try:
+            traffic = json.loads(prof_json.read_text()).get("element_kernel_dram_bytes")
+        except (ValueError, OSError):
+            traffic = None
+
+    # ---- end-to-end through the public API (pinned host buffers) -------------
+    u_pin = torch.empty(prob["zhat"], dtype=torch.float64, pin_memory=True)
+    u_pin.copy_(torch.from_numpy(prob["uhat"]))
+    u_host = u_pin.numpy()
+    e2e_steps = max(3, min(args.steps, 200))
+    for _ in range(2):
+        P.apply_schur(sys_, u_host)
+    barrier(world)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        w_host = P.apply_schur(sys_, u_host)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    e2e_wall = time.perf_counter() - t0
+    e2e_ms = max_over_ranks(max(e0.elapsed_time(e1), e2e_wall * 1e3) / e2e_steps, world)
+    assert w_host.shape == (prob["zhat"],)
+
+    # ---- full solve (GMRES + D^-1 to 1e-10) ----------------------------------
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    x, info = P.gmres(P.SchurOperator(sys_), sys_.f_device, cfg, precond=P.Preconditioner(sys_))
+    torch.cuda.synchronize(dev)
+    t_solve = time.perf_counter() - t0
+
+    line = {
+        "metric": BASELINE_METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded BASELINE generator, numpy PCG64; blocks resident in HBM)",
+        "config": config_block(args.config, prob, world),
+        "hbm_gbs": bytes_apply / (ms_per_step * 1e-3) / 1e9,
+        "hbm_frac": bytes_apply / (ms_per_step * 1e-3) / 1e9 / peaks["hbm_gbs"],
+        "bytes_per_apply": bytes_apply,
+        "roofline": {"bound": "hbm", "kernel": "element_kernel (gather+B^T+LU solve+C, per macro)",
+                     "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                     "algorithmic_bytes_per_launch": elem_bytes, "avg_launch_ms": elem_avg_ms,
+                     "face_kernel_avg_ms": face_avg_ms, "peak_source": peaks["source"]},
+        "e2e": {"value": 1e3 / e2e_ms, "unit": UNIT, "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": prob["zhat"] * 8, "d2h_bytes_per_step": prob["zhat"] * 8,
+                "api": "paper_2302_10917_b200.apply_schur(sys, numpy pinned uhat)"},
+        "gpu_launches": int(el_n.value + fa_n.value),
+        "lu": {"gflops": lu_flops / (lu_ms * 1e-3) / 1e9, "ms": lu_ms, "flops": lu_flops,
+               "bytes": 16 * N * Q * Q, "gbs": 16 * N * Q * Q / (lu_ms * 1e-3) / 1e9},
+        "solve": {"iterations": info["iterations"], "converged": info["converged"],
+                  "seconds": t_solve, "tol": 1e-10},
+        "setup_s": {"generate": t_gen, "condense": t_condense},
+        "clocks": sampler.summary(),
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        cb = time_oracle(prob, args.cpu_sample, reps=args.cpu_reps, threads=1)
+        line["cpu_baseline"] = {
+            "value": cb["applies_per_s"], "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": (f"oracle port (per-macro scipy LAPACK loop) on macros [0,"
+                       f"{cb['sample_macros']}) + {cb['sample_faces']} faces, mean of "
+                       f"{cb['reps']} applies x{cb['scale']:.1f}"),
+            "lu_gflops": cb["lu_gflops"]}
+    if rank == 0:
+        print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-sample", type=int, default=2048)
+    ap.add_argument("--cpu-reps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world, rank, local = (1, 0, 0)
+    if args.impl == "reference":
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        rank = int(os.environ.get("RANK", "0"))
+        return run_reference(args, world, rank)
+    world, rank, local = dist_setup()
+    try:
+        return run_ours(args, world, rank, local)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -163,6 +163,15 @@ int mh_apply_mb(mh_system* sys, const double* uhat_dev, double* w_dev);
  * macros [first, first+count): out_host[count*nc*nc] row-major. */
 int mh_get_element_schur(mh_system* sys, int64_t first, int64_t count, double* out_host);
 
+/* ---- per-kernel timing (CUDA events around each launch) ---------------- */
+/* enable != 0 starts recording events around the element and face kernels
+ * launched by the operator entry points; mh_profile_read synchronises the
+ * stream, returns the summed durations (ms) and launch counts since the last
+ * read, and clears them. */
+int mh_profile(mh_system* sys, int enable);
+int mh_profile_read(mh_system* sys, double* elem_ms, int64_t* elem_launches,
+                    double* face_ms, int64_t* face_launches);
+
 /* ---- GMRES (schur_solver.py:308-385) ----------------------------------- */
 
 /* Operator callback: out_dev = Op(in_dev), both n doubles on the device. */

@@ -31,6 +31,64 @@ extern "C" int mh_device_count(int* count) {
   return MH_OK;
 }
 
+namespace mh {
+static cudaEvent_t take_event(mh_system* s) {
+  if (!s->ev_pool.empty()) {
+    cudaEvent_t e = s->ev_pool.back();
+    s->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+int prof_begin(mh_system* s, cudaEvent_t* ev) {
+  *ev = nullptr;
+  if (!s->profiling) return MH_OK;
+  *ev = take_event(s);
+  MH_CHECK_CUDA(cudaEventRecord(*ev, s->stream));
+  return MH_OK;
+}
+int prof_end(mh_system* s, cudaEvent_t ev0, int kind) {
+  if (!s->profiling || !ev0) return MH_OK;
+  cudaEvent_t ev1 = take_event(s);
+  MH_CHECK_CUDA(cudaEventRecord(ev1, s->stream));
+  (kind == 0 ? s->ev_elem : s->ev_face).emplace_back(ev0, ev1);
+  return MH_OK;
+}
+}  // namespace mh
+
+extern "C" int mh_profile(mh_system* s, int enable) {
+  if (!s) return MH_E_ARG;
+  s->profiling = enable != 0;
+  return MH_OK;
+}
+
+extern "C" int mh_profile_read(mh_system* s, double* elem_ms, int64_t* elem_n, double* face_ms,
+                               int64_t* face_n) {
+  if (!s) return MH_E_ARG;
+  MH_CHECK_CUDA(cudaStreamSynchronize(s->stream));
+  double sums[2] = {0.0, 0.0};
+  int64_t counts[2] = {0, 0};
+  for (int k = 0; k < 2; ++k) {
+    auto& v = k == 0 ? s->ev_elem : s->ev_face;
+    for (auto& pr : v) {
+      float ms = 0.f;
+      MH_CHECK_CUDA(cudaEventElapsedTime(&ms, pr.first, pr.second));
+      sums[k] += ms;
+      counts[k] += 1;
+      s->ev_pool.push_back(pr.first);
+      s->ev_pool.push_back(pr.second);
+    }
+    v.clear();
+  }
+  if (elem_ms) *elem_ms = sums[0];
+  if (elem_n) *elem_n = counts[0];
+  if (face_ms) *face_ms = sums[1];
+  if (face_n) *face_n = counts[1];
+  return MH_OK;
+}
+
 static int need(mh_system* s, bool cond, const char* msg) {
   if (!s) {
     set_error("null system");
@@ -81,13 +139,17 @@ extern "C" int mh_destroy(mh_system* s) {
   cudaSetDevice(s->device);
   if (s->stream) cudaStreamSynchronize(s->stream);
   s->elem_ufac.release(); s->face_vslot.release();
-  s->A.release(); s->LU.release(); s->dinv.release(); s->piv.release(); s->perm.release();
+  s->A.release(); s->LU.release(); s->Lp.release(); s->Up.release(); s->udiag.release();
+  s->dinv.release(); s->piv.release(); s->perm.release();
   s->lstat.release(); s->Bt.release(); s->Cm.release(); s->Ru.release(); s->D.release();
   s->Draw.release(); s->Rhat.release(); s->FL.release(); s->FU.release(); s->FrL.release();
   s->FrU.release(); s->Fperm.release(); s->Fsign.release(); s->Fkind.release(); s->V.release();
   s->tmp.release(); s->S.release(); s->halo_u.release(); s->hin.release(); s->hout.release();
   if (s->kry) free_krylov(s->kry);
   free_comm(s);
+  for (auto& pr : s->ev_elem) { s->ev_pool.push_back(pr.first); s->ev_pool.push_back(pr.second); }
+  for (auto& pr : s->ev_face) { s->ev_pool.push_back(pr.first); s->ev_pool.push_back(pr.second); }
+  for (cudaEvent_t e : s->ev_pool) cudaEventDestroy(e);
   if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
   delete s;
   return MH_OK;
@@ -150,13 +212,18 @@ extern "C" int mh_upload_connectivity(mh_system* s, const int32_t* elem_ufac,
 
 static int alloc_blocks(mh_system* s) {
   const size_t N = (size_t)s->N, Q = s->Q, nc = s->nc, F = (size_t)s->F, t = s->t;
+  s->ldB = ((int64_t)nc * Q + 1) & ~(int64_t)1;
+  s->ldL = ((int64_t)Q * (Q - 1) / 2 + 1) & ~(int64_t)1;
+  if (s->ldL < 2) s->ldL = 2;
   MH_CHECK(s->A.alloc(N * Q * Q));
-  MH_CHECK(s->LU.alloc(N * Q * Q));
+  MH_CHECK(s->Lp.alloc(N * (size_t)s->ldL));
+  MH_CHECK(s->Up.alloc(N * (size_t)s->ldL));
+  MH_CHECK(s->udiag.alloc(N * Q));
   MH_CHECK(s->dinv.alloc(N * Q));
   MH_CHECK(s->piv.alloc(N * Q));
   MH_CHECK(s->perm.alloc(N * Q));
   MH_CHECK(s->lstat.alloc(N));
-  MH_CHECK(s->Bt.alloc(N * nc * Q));
+  MH_CHECK(s->Bt.alloc(N * (size_t)s->ldB));
   MH_CHECK(s->Ru.alloc(N * Q));
   MH_CHECK(s->D.alloc(F * t * t));
   MH_CHECK(s->Draw.alloc(F * t * t));
@@ -186,24 +253,27 @@ static int upload_impl(mh_system* s, const double* A, const double* B, const dou
   cudaStream_t st = s->stream;
   if (N) MH_CHECK_CUDA(cudaMemcpyAsync(s->A.p, A, sizeof(double) * N * Q * Q, kind, st));
   s->c_is_bt = (B == nullptr) || (C == nullptr);
-  if (!s->c_is_bt) MH_CHECK(s->Cm.alloc(N * nc * Q));
+  if (!s->c_is_bt) MH_CHECK(s->Cm.alloc(N * (size_t)s->ldB));
   else s->Cm.release();
+  const size_t row = sizeof(double) * nc * Q, pitch = sizeof(double) * (size_t)s->ldB;
+  if (N && (s->ldB & 1) == 0 && (size_t)s->ldB != nc * Q)  // zero the per-macro pad
+    MH_CHECK_CUDA(cudaMemsetAsync(s->Bt.p, 0, pitch * N, st));
   if (B == nullptr) {
-    if (N) MH_CHECK_CUDA(cudaMemcpyAsync(s->Bt.p, C, sizeof(double) * N * nc * Q, kind, st));
+    if (N) MH_CHECK_CUDA(cudaMemcpy2DAsync(s->Bt.p, pitch, C, row, row, N, kind, st));
   } else {
-    // op.B (N x Q x nc) -> Bt (N x nc x Q), staged through LU's storage
+    // op.B (N x Q x nc) -> Bt (N x nc x Q, stride ldB) through a staging buffer
     if (N) {
-      double* stage = s->LU.p;
-      if (nc > Q) {  // LU slot is too small: use a temporary
-        MH_CHECK(s->S.alloc(N * nc * Q));
-        stage = s->S.p;
-      }
-      MH_CHECK_CUDA(cudaMemcpyAsync(stage, B, sizeof(double) * N * nc * Q, kind, st));
-      MH_CHECK(launch_transpose_batched(st, stage, s->Bt.p, (int64_t)N, (int)Q, (int)nc));
+      MH_CHECK(s->S.alloc(N * nc * Q));
+      MH_CHECK_CUDA(cudaMemcpyAsync(s->S.p, B, row * N, kind, st));
+      MH_CHECK(launch_transpose_batched(st, s->S.p, s->Bt.p, (int64_t)N, (int)Q, (int)nc,
+                                        s->ldB));
       MH_CHECK_CUDA(cudaStreamSynchronize(st));
-      if (stage == s->S.p) s->S.release();
+      s->S.release();
     }
-    if (C && N) MH_CHECK_CUDA(cudaMemcpyAsync(s->Cm.p, C, sizeof(double) * N * nc * Q, kind, st));
+    if (C && N) {
+      MH_CHECK_CUDA(cudaMemsetAsync(s->Cm.p, 0, pitch * N, st));
+      MH_CHECK_CUDA(cudaMemcpy2DAsync(s->Cm.p, pitch, C, row, row, N, kind, st));
+    }
   }
   if (N) {
     if (Ru) MH_CHECK_CUDA(cudaMemcpyAsync(s->Ru.p, Ru, sizeof(double) * N * Q, kind, st));
@@ -286,8 +356,8 @@ extern "C" int mh_get_local_factors(mh_system* s, int64_t first, int64_t count, 
   if (lu_host && count) {
     DBuf<double> tmp;
     MH_CHECK(tmp.alloc(QQ * count));
-    // column-major device factors -> row-major host (scipy's lu[i, j])
-    MH_CHECK(launch_transpose_batched(s->stream, s->LU.p + first * QQ, tmp.p, count, s->Q, s->Q));
+    // packed device factors -> row-major host (scipy's lu[i, j])
+    MH_CHECK(launch_unpack_lu(s, first, count, tmp.p));
     MH_CHECK_CUDA(cudaMemcpyAsync(lu_host, tmp.p, sizeof(double) * QQ * count,
                                   cudaMemcpyDeviceToHost, s->stream));
     MH_CHECK_CUDA(cudaStreamSynchronize(s->stream));
@@ -320,17 +390,27 @@ extern "C" int mh_rhs(mh_system* s, double* f) {
 extern "C" int mh_apply(mh_system* s, const double* u, double* w) {
   MH_CHECK(ready(s));
   MH_CHECK(halo_u_exchange(s, u, nullptr));
+  cudaEvent_t ev;
+  MH_CHECK(prof_begin(s, &ev));
   MH_CHECK(launch_element(s, kApply, u, s->V.p));
+  MH_CHECK(prof_end(s, ev, 0));
   MH_CHECK(halo_v_exchange(s));
-  return launch_face_reduce(s, u, w, 0, 0);
+  MH_CHECK(prof_begin(s, &ev));
+  MH_CHECK(launch_face_reduce(s, u, w, 0, 0));
+  return prof_end(s, ev, 1);
 }
 
 extern "C" int mh_apply_precond(mh_system* s, const double* u, double* z) {
   MH_CHECK(ready(s));
   MH_CHECK(halo_u_exchange(s, u, nullptr));
+  cudaEvent_t ev;
+  MH_CHECK(prof_begin(s, &ev));
   MH_CHECK(launch_element(s, kApply, u, s->V.p));
+  MH_CHECK(prof_end(s, ev, 0));
   MH_CHECK(halo_v_exchange(s));
-  return launch_face_reduce(s, u, z, 0, 1);
+  MH_CHECK(prof_begin(s, &ev));
+  MH_CHECK(launch_face_reduce(s, u, z, 0, 1));
+  return prof_end(s, ev, 1);
 }
 
 extern "C" int mh_precond(mh_system* s, const double* w, double* z) {

@@ -1,116 +1,61 @@
-// Fused per-macro element kernel: one warp per macro-element.
+// Fused per-macro element kernel: one warp per macro, persistent warps fed
+// by a TMA bulk-copy stream (stream.cuh).
 //
 // Replaces the macro_task of apply_schur (schur_solver.py:271-277),
 // macro_rhs of condense (:244-246) and the reconstruct_interior task
 // (:426-429).  Per macro e, with lane l owning rows i = l + 32 r:
 //   gather   ue = uhat through the face table (zeros on Dirichlet slots)
 //   step 1   x  = P (B ue)        B = op.B, streamed as op.B^T rows (nc x Q)
-//   step 2   y  = U^-1 L^-1 x     column-oriented substitution, warp shuffles
+//   step 2   y  = U^-1 L^-1 x     column-oriented substitution with warp
+//                                 shuffles; L and U are streamed as packed
+//                                 column segments (forward: L columns
+//                                 0..Q-2, backward: U columns Q-1..1)
 //   step 3   v  = C y             op.C rows, 32-row transpose-reduce
 //   write    V[e*nc + c]          the macro's slot segment; the face kernel
 //                                 subtracts it in left-then-right order, so
-//                                 there are no atomics and results are
+//                                 there are no atomics and the result is
 //                                 deterministic.
 // Modes: kApply (above), kRhs (x = P R_u, writes v), kRecon
 // (x = P (R_u - B ue), writes y = u_e).
-// All block data is streamed exactly once per launch with
-// ld.global.nc.L1::no_allocate; only op.C is read a second time (when
-// op.C = op.B^T the step-3 read hits the L2 lines step 1 brought in, which
-// are loaded with an evict_last policy).
+//
+// HBM traffic per macro = 8 (nc Q [B] + Q(Q-1) [L,U] + nc Q [C]) + small
+// vectors.  When op.C = op.B^T (the BASELINE operator) the C segment is the
+// same memory as the B segment; it is fetched with an L2 evict_last policy
+// on its first read so the second read is served from L2.
+//
+// The kernel is issue-bound once the stream keeps HBM busy, so the loops
+// are written for instruction count: rows / columns are consumed in groups
+// of four behind one ring-window check, and a group that does not wrap
+// around the ring end is read with immediate-offset shared loads.
 
 #include "mh_internal.h"
+#include "stream.cuh"
 
 namespace mh {
 namespace {
 
-constexpr int kElemWarps = 4;  // warps (macros) per CTA
-
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t p;
-  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t policy_evict_last() {
-  uint64_t p;
-  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-// streaming read: no L1 allocation, L2 evict-first
-__device__ __forceinline__ double ld_stream(const double* p) {
-  double v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
-               : "=d"(v) : "l"(p), "l"(policy_evict_first()));
-  return v;
-}
-// read that will be repeated by this warp shortly: keep in L2
-__device__ __forceinline__ double ld_keep(const double* p) {
-  double v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
-               : "=d"(v) : "l"(p), "l"(policy_evict_last()));
-  return v;
-}
+constexpr int kWPB = 4;        // warps (pipelines) per CTA
+constexpr int kRingD = 2048;   // doubles per warp ring (16 KB)
+constexpr int kChunk = 256;    // doubles per bulk-copy chunk (2 KB)
+using RingT = Ring<kRingD, kChunk>;
+constexpr uint32_t kM = RingT::M;
 
 struct ElemArgs {
   const int32_t* elem_ufac;
   const double* uhat;
   const double* uhalo;  // received halo segments (trace index >= F)
-  const double* Bt;
-  const double* Cm;
-  const double* LU;
+  const double* Bt;     // N x ldB   (op.B^T rows, nc x Q)
+  const double* Cm;     // N x ldB   (op.C rows,   nc x Q)
+  const double* Lp;     // N x ldL   packed strict lower, columns 0..Q-2
+  const double* Up;     // N x ldL   packed strict upper, columns Q-1..1
   const double* dinv;
   const int32_t* perm;
   const double* Ru;
   double* out;
-  int64_t N, F;
+  int64_t N, F, ldB, ldL;
   int Q, nc, t, nfe;
   int c_is_bt;
 };
-
-// Unit-lower forward substitution, column-oriented: at step j the lane that
-// owns row j broadcasts y_j and every row i > j does y_i -= L_ij y_j.
-template <int R>
-__device__ __forceinline__ void forward_unit_lower(double (&y)[R], const double* __restrict__ LUe,
-                                                   int Q, int lane) {
-#pragma unroll
-  for (int jb = 0; jb < R; ++jb) {
-#pragma unroll 4
-    for (int jj = 0; jj < 32; ++jj) {
-      const int j = jb * 32 + jj;
-      if (j < Q - 1) {
-        const double yj = __shfl_sync(kFull, y[jb], jj);
-        const double* col = LUe + (size_t)j * Q;
-#pragma unroll
-        for (int r = jb; r < R; ++r) {
-          const int i = lane + 32 * r;
-          if (i > j && i < Q) y[r] = fma(-ld_stream(col + i), yj, y[r]);
-        }
-      }
-    }
-  }
-}
-
-// Upper back substitution with the stored reciprocal diagonal.
-template <int R>
-__device__ __forceinline__ void backward_upper(double (&y)[R], const double* __restrict__ LUe,
-                                               const double (&dr)[R], int Q, int lane) {
-#pragma unroll
-  for (int jb = R - 1; jb >= 0; --jb) {
-#pragma unroll 4
-    for (int jj = 31; jj >= 0; --jj) {
-      const int j = jb * 32 + jj;
-      if (j < Q) {
-        if (lane == jj) y[jb] *= dr[jb];
-        const double yj = __shfl_sync(kFull, y[jb], jj);
-        const double* col = LUe + (size_t)j * Q;
-#pragma unroll
-        for (int r = 0; r <= jb; ++r) {
-          const int i = lane + 32 * r;
-          if (i < j) y[r] = fma(-ld_stream(col + i), yj, y[r]);
-        }
-      }
-    }
-  }
-}
 
 // 32 per-lane partial sums -> lane l holds the full sum of partial l
 // (butterfly transpose-reduce: 31 shuffles for 32 sums).
@@ -128,148 +73,324 @@ __device__ __forceinline__ double transpose_reduce32(double (&p)[32], int lane) 
   return p[0];
 }
 
+__device__ __forceinline__ bool no_wrap(uint32_t lo, uint32_t span) {
+  return (lo & kM) + span <= (uint32_t)kRingD;
+}
+
+// x_i += sum over 4 rows c of op.B^T[c][perm_i] * ue_c, rows at stream p, p+Q, ...
+template <int R, bool WRAP, bool PERM>
+__device__ __forceinline__ void gemv_rows4(double (&acc)[R], const double* ring, uint32_t p,
+                                           int nrow, int Q, const double* su, const int (&pr)[R],
+                                           int lane) {
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    if (u < nrow) {
+      const double uc = su[u];
+      const double* cb = ring + (p & kM);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int i = PERM ? pr[r] : lane + 32 * r;
+        const double b = WRAP ? ring[(p + (uint32_t)i) & kM] : cb[i];
+        if (lane + 32 * r < Q) acc[r] = fma(b, uc, acc[r]);
+      }
+      p += Q;
+    }
+  }
+}
+
+// forward substitution over 4 packed L columns j0..j0+3 (JB = j0 / 32 is a
+// compile-time constant once the caller's block loop is unrolled)
+template <int R, bool WRAP>
+__device__ __forceinline__ void fwd_cols4(double (&y)[R], const double* ring, uint32_t p, int JB,
+                                          int j0, int Q, int lane) {
+  const int jj0 = j0 & 31;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int j = j0 + u;
+    if (j < Q - 1) {
+      const uint32_t q0 = p - (uint32_t)(j + 1);  // stream position of "row 0"
+      const double yj = __shfl_sync(kFull, y[JB], jj0 + u);
+      const double* cb = ring + (q0 & kM);
+#pragma unroll
+      for (int r = JB; r < R; ++r) {
+        const int i = lane + 32 * r;
+        const double l = WRAP ? ring[(q0 + (uint32_t)i) & kM] : cb[i];
+        if (r > JB || lane > jj0 + u) y[r] = fma(-l, yj, y[r]);
+      }
+      p += (uint32_t)(Q - 1 - j);
+    }
+  }
+}
+
+// back substitution over 4 packed U columns j0, j0-1, .. (descending; JB = j0 / 32)
+template <int R, bool WRAP>
+__device__ __forceinline__ void bwd_cols4(double (&y)[R], const double (&dr)[R],
+                                          const double* ring, uint32_t p, int JB, int j0,
+                                          int lane) {
+  const int jj0 = j0 & 31;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int j = j0 - u;
+    if (j >= JB * 32) {
+      if (lane == jj0 - u) y[JB] *= dr[JB];
+      const double yj = __shfl_sync(kFull, y[JB], jj0 - u);
+      const double* cb = ring + (p & kM);
+#pragma unroll
+      for (int r = 0; r <= JB; ++r) {
+        const int i = lane + 32 * r;
+        const double uv = WRAP ? ring[(p + (uint32_t)i) & kM] : cb[i];
+        if (r < JB || lane < jj0 - u) y[r] = fma(-uv, yj, y[r]);
+      }
+      p += (uint32_t)j;
+    }
+  }
+}
+
+// partial dot products of 4 op.C rows with y (rows at p, p+Q, ...) into pp[Q0..Q0+3]
+template <int R, bool WRAP>
+__device__ __forceinline__ void dot_rows4(double (&pp)[32], int Q0, const double (&y)[R],
+                                          const double* ring, uint32_t p, int nrow, int Q,
+                                          int lane) {
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    double acc = 0.0;
+    if (u < nrow) {
+      const double* cb = ring + (p & kM);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int i = lane + 32 * r;
+        const double c = WRAP ? ring[(p + (uint32_t)i) & kM] : cb[i];
+        if (i < Q) acc = fma(c, y[r], acc);
+      }
+      p += Q;
+    }
+    pp[Q0 + u] = acc;
+  }
+}
+
 template <int R, int MODE>
-__global__ void __launch_bounds__(kElemWarps * 32)
+__global__ void __launch_bounds__(kWPB * 32, 3)
 element_kernel(ElemArgs a) {
-  extern __shared__ double s_u[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ Segment segs[4];
+  __shared__ RingState rst[kWPB];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t e = (int64_t)blockIdx.x * kElemWarps + w;
-  if (e >= a.N) return;  // warp-uniform; no CTA-wide barriers below
   const int Q = a.Q, nc = a.nc, t = a.t;
-  const size_t QQ = (size_t)Q * Q;
-  const size_t CQ = (size_t)nc * Q;
-
-  int pr[R];
-  double dr[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int i = lane + 32 * r;
-    pr[r] = i < Q ? __ldg(a.perm + e * Q + i) : 0;
-    dr[r] = i < Q ? __ldg(a.dinv + e * Q + i) : 0.0;
+  const int lenB = (int)(((int64_t)nc * Q + 1) & ~1);
+  const int lenL = (int)(((int64_t)Q * (Q - 1) / 2 + 1) & ~1);
+  int nseg = 0;
+  if (MODE != kRhs) ++nseg;
+  nseg += 2;
+  if (MODE != kRecon) ++nseg;
+  if (threadIdx.x == 0) {
+    int n = 0;
+    if (MODE != kRhs) segs[n++] = Segment{a.Bt, a.ldB, lenB, (MODE == kApply && a.c_is_bt) ? 1 : 0};
+    segs[n++] = Segment{a.Lp, a.ldL, lenL, 0};
+    segs[n++] = Segment{a.Up, a.ldL, lenL, 0};
+    if (MODE != kRecon) segs[n++] = Segment{a.Cm, a.ldB, lenB, 0};
   }
+  __syncthreads();  // the only CTA-wide barrier
+  double* ring = reinterpret_cast<double*>(smem_raw) + (size_t)w * kRingD;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<double*>(smem_raw) +
+                                               (size_t)kWPB * kRingD) + w * RingT::S;
+  double* su = reinterpret_cast<double*>(reinterpret_cast<uint64_t*>(
+                   reinterpret_cast<double*>(smem_raw) + (size_t)kWPB * kRingD) +
+               kWPB * RingT::S) + (size_t)w * ((nc + 3) & ~3);
 
-  double y[R];
-  if (MODE == kRhs) {
-#pragma unroll
-    for (int r = 0; r < R; ++r) y[r] = (lane + 32 * r < Q) ? __ldg(a.Ru + e * Q + pr[r]) : 0.0;
-  } else {
-    double* su = s_u + w * nc;
-    const int32_t* ef = a.elem_ufac + e * a.nfe;
-    for (int c = lane; c < nc; c += 32) {
-      const int k = c / t, s = c - k * t;
-      const int f = __ldg(ef + k);
-      su[c] = f < 0 ? 0.0
-              : (f < a.F ? __ldg(a.uhat + (int64_t)f * t + s)
-                         : __ldg(a.uhalo + (int64_t)(f - a.F) * t + s));
-    }
-    __syncwarp();
-    double acc[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) acc[r] = 0.0;
-    const double* Bte = a.Bt + e * CQ;
-#pragma unroll 4
-    for (int c = 0; c < nc; ++c) {
-      const double uc = su[c];
-      const double* row = Bte + (size_t)c * Q;
-#pragma unroll
-      for (int r = 0; r < R; ++r)
-        if (lane + 32 * r < Q) {
-          const double b = (MODE == kApply && a.c_is_bt) ? ld_keep(row + pr[r]) : ld_stream(row + pr[r]);
-          acc[r] = fma(b, uc, acc[r]);
-        }
-    }
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      if (MODE == kApply) y[r] = acc[r];
-      else y[r] = (lane + 32 * r < Q) ? __ldg(a.Ru + e * Q + pr[r]) - acc[r] : 0.0;
-    }
-  }
+  const int64_t gw = (int64_t)blockIdx.x * kWPB + w;
+  const int64_t W = (int64_t)gridDim.x * kWPB;
+  const uint32_t offL = (MODE != kRhs) ? (uint32_t)lenB : 0u;
+  const uint32_t offU = offL + (uint32_t)lenL;
+  const uint32_t offC = offU + (uint32_t)lenL;
+  const uint32_t E = offC + ((MODE != kRecon) ? (uint32_t)lenB : 0u);
+  RingState* st = &rst[w];
+  RingT::init(st, lane, ring, bars, segs, nseg, gw, W, a.N, E);
+  uint32_t ready = 0;
+#define MH_WINDOW(A_, B_) \
+  if ((B_) > ready) ready = RingT::slow(st, (A_), (B_), lane)
 
-  const double* LUe = a.LU + e * QQ;
-  forward_unit_lower<R>(y, LUe, Q, lane);
-  backward_upper<R>(y, LUe, dr, Q, lane);
-
-  if (MODE == kRecon) {
+  uint32_t base = 0;
+  for (int64_t e = gw; e < a.N; e += W, base += E) {
+    int pr[R];
+    double dr[R];
+    bool ident = true;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int i = lane + 32 * r;
-      if (i < Q) a.out[e * Q + i] = y[r];
+      pr[r] = i < Q ? __ldg(a.perm + e * Q + i) : i;
+      dr[r] = i < Q ? __ldg(a.dinv + e * Q + i) : 0.0;
+      ident = ident && pr[r] == i;
     }
-    return;
-  }
-
-  // step 3: v_c = sum_i C[c][i] y_i
-  const double* Ce = a.Cm + e * CQ;
-  for (int c0 = 0; c0 < nc; c0 += 32) {
-    double pp[32];
+    const bool has_perm = !__all_sync(kFull, ident);
+    double y[R];
+    if (MODE == kRhs) {
 #pragma unroll
-    for (int q = 0; q < 32; ++q) {
-      double acc = 0.0;
-      const int c = c0 + q;
-      if (c < nc) {
-        const double* row = Ce + (size_t)c * Q;
-#pragma unroll
-        for (int r = 0; r < R; ++r)
-          if (lane + 32 * r < Q) acc = fma(ld_stream(row + lane + 32 * r), y[r], acc);
+      for (int r = 0; r < R; ++r) y[r] = (lane + 32 * r < Q) ? __ldg(a.Ru + e * Q + pr[r]) : 0.0;
+    } else {
+      const int32_t* ef = a.elem_ufac + e * a.nfe;
+      for (int c = lane; c < nc; c += 32) {
+        const int k = c / t, s = c - k * t;
+        const int f = __ldg(ef + k);
+        su[c] = f < 0 ? 0.0
+                : (f < a.F ? __ldg(a.uhat + (int64_t)f * t + s)
+                           : __ldg(a.uhalo + (int64_t)(f - a.F) * t + s));
       }
-      pp[q] = acc;
+      __syncwarp();
+      double acc[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc[r] = 0.0;
+      uint32_t p = base;
+      for (int c = 0; c < nc; c += 4, p += 4u * (uint32_t)Q) {  // step 1: x = B ue
+        const int nrow = min(4, nc - c);
+        const uint32_t span = (uint32_t)(nrow * Q);
+        MH_WINDOW(p, p + span);
+        if (no_wrap(p, span + 32u * R)) {
+          if (has_perm) gemv_rows4<R, false, true>(acc, ring, p, nrow, Q, su + c, pr, lane);
+          else gemv_rows4<R, false, false>(acc, ring, p, nrow, Q, su + c, pr, lane);
+        } else {
+          gemv_rows4<R, true, true>(acc, ring, p, nrow, Q, su + c, pr, lane);
+        }
+      }
+      __syncwarp();  // su is rewritten by the next macro
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (MODE == kApply) y[r] = acc[r];
+        else y[r] = (lane + 32 * r < Q) ? __ldg(a.Ru + e * Q + pr[r]) - acc[r] : 0.0;
+      }
     }
-    const double v = transpose_reduce32(pp, lane);
-    if (c0 + lane < nc) a.out[e * nc + c0 + lane] = v;
+
+    // step 2a: unit-lower forward substitution over packed L columns
+    {
+      uint32_t p = base + offL;
+#pragma unroll
+      for (int jb = 0; jb < R; ++jb) {
+        const int jend = min(jb * 32 + 32, Q - 1);
+        for (int j0 = jb * 32; j0 < jend; j0 += 4) {
+          const int ncol = min(4, jend - j0);
+          const uint32_t span = (uint32_t)(ncol * (Q - 1 - j0) - ncol * (ncol - 1) / 2);
+          MH_WINDOW(p, p + span);
+          if (no_wrap(p - (uint32_t)(j0 + 1), span + (uint32_t)(j0 + 1) + 32u * R + 8u))
+            fwd_cols4<R, false>(y, ring, p, jb, j0, Q, lane);
+          else
+            fwd_cols4<R, true>(y, ring, p, jb, j0, Q, lane);
+          p += span;
+        }
+      }
+    }
+    // step 2b: upper back substitution over packed U columns Q-1 .. 0 (column
+    // 0 has no strictly-upper entries, only the diagonal)
+    {
+      uint32_t p = base + offU;
+#pragma unroll
+      for (int jb = R - 1; jb >= 0; --jb) {
+        for (int j0 = min(jb * 32 + 31, Q - 1); j0 >= jb * 32; j0 -= 4) {
+          const int ncol = min(4, j0 - jb * 32 + 1);
+          const uint32_t span = (uint32_t)(ncol * j0 - ncol * (ncol - 1) / 2);
+          MH_WINDOW(p, p + span);
+          if (no_wrap(p, span + 32u * R + 8u))
+            bwd_cols4<R, false>(y, dr, ring, p, jb, j0, lane);
+          else
+            bwd_cols4<R, true>(y, dr, ring, p, jb, j0, lane);
+          p += span;
+        }
+      }
+    }
+
+    if (MODE == kRecon) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int i = lane + 32 * r;
+        if (i < Q) a.out[e * Q + i] = y[r];
+      }
+      continue;
+    }
+
+    // step 3: v_c = sum_i C[c][i] y_i, 32 rows per transpose-reduce
+    uint32_t p = base + offC;
+    for (int c0 = 0; c0 < nc; c0 += 32) {
+      double pp[32];
+#pragma unroll
+      for (int q0 = 0; q0 < 32; q0 += 4) {
+        const int nrow = max(0, min(4, nc - c0 - q0));
+        const uint32_t span = (uint32_t)(nrow * Q);
+        if (nrow > 0) MH_WINDOW(p, p + span);
+        if (no_wrap(p, span + 32u * R))
+          dot_rows4<R, false>(pp, q0, y, ring, p, nrow, Q, lane);
+        else
+          dot_rows4<R, true>(pp, q0, y, ring, p, nrow, Q, lane);
+        p += span;
+      }
+      const double v = transpose_reduce32(pp, lane);
+      if (c0 + lane < nc) a.out[e * nc + c0 + lane] = v;
+    }
   }
+#undef MH_WINDOW
+}
+
+size_t smem_bytes(int nc) {
+  return (size_t)kWPB * kRingD * sizeof(double) + (size_t)kWPB * RingT::S * sizeof(uint64_t) +
+         (size_t)kWPB * ((nc + 3) & ~3) * sizeof(double);
+}
+
+template <int R, int MODE>
+int launch_rm(mh_system* s, const ElemArgs& a) {
+  const size_t smem = smem_bytes(s->nc);
+  auto kern = element_kernel<R, MODE>;
+  MH_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  MH_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWPB * 32, smem));
+  if (per_sm < 1) per_sm = 1;
+  int64_t grid = (int64_t)s->num_sms * per_sm;
+  const int64_t need = (s->N + kWPB - 1) / kWPB;
+  if (grid > need) grid = need;
+  kern<<<(unsigned)grid, kWPB * 32, smem, s->stream>>>(a);
+  MH_CHECK_CUDA(cudaGetLastError());
+  return MH_OK;
 }
 
 template <int MODE>
 int launch_mode(mh_system* s, const double* uhat, double* out) {
+  if (s->N == 0) return MH_OK;
   ElemArgs a;
   a.elem_ufac = s->elem_ufac.p;
   a.uhat = uhat;
   a.uhalo = s->halo_u.p;
   a.Bt = s->Bt.p;
   a.Cm = s->c_is_bt ? s->Bt.p : s->Cm.p;
-  a.LU = s->LU.p;
+  a.Lp = s->Lp.p;
+  a.Up = s->Up.p;
   a.dinv = s->dinv.p;
   a.perm = s->perm.p;
   a.Ru = s->Ru.p;
   a.out = out;
   a.N = s->N;
   a.F = s->F;
+  a.ldB = s->ldB;
+  a.ldL = s->ldL;
   a.Q = s->Q;
   a.nc = s->nc;
   a.t = s->t;
   a.nfe = s->nfe;
   a.c_is_bt = s->c_is_bt ? 1 : 0;
-  if (s->N == 0) return MH_OK;
-  const unsigned grid = (unsigned)((s->N + kElemWarps - 1) / kElemWarps);
-  const size_t smem = (size_t)kElemWarps * s->nc * sizeof(double);
-  const int R = (s->Q + 31) / 32;
-  switch (R) {
-#define MH_ELEM_CASE(RR)                                                              \
-  case RR:                                                                            \
-    element_kernel<RR, MODE><<<grid, kElemWarps * 32, smem, s->stream>>>(a);          \
-    break;
-    MH_ELEM_CASE(1)
-    MH_ELEM_CASE(2)
-    MH_ELEM_CASE(3)
-    MH_ELEM_CASE(4)
-    MH_ELEM_CASE(5)
-    MH_ELEM_CASE(6)
-    MH_ELEM_CASE(7)
-    MH_ELEM_CASE(8)
-#undef MH_ELEM_CASE
-    default:
-      set_error("element kernel: Q > 256 unsupported");
-      return MH_E_UNSUPPORTED;
+  switch ((s->Q + 31) / 32) {
+    case 1: return launch_rm<1, MODE>(s, a);
+    case 2: return launch_rm<2, MODE>(s, a);
+    case 3: return launch_rm<3, MODE>(s, a);
+    case 4: return launch_rm<4, MODE>(s, a);
+    case 5: return launch_rm<5, MODE>(s, a);
+    case 6: return launch_rm<6, MODE>(s, a);
+    case 7: return launch_rm<7, MODE>(s, a);
+    case 8: return launch_rm<8, MODE>(s, a);
   }
-  MH_CHECK_CUDA(cudaGetLastError());
-  return MH_OK;
+  set_error("element kernel: Q > 256 unsupported");
+  return MH_E_UNSUPPORTED;
 }
 
 }  // namespace
 
 int launch_element(mh_system* s, int mode, const double* uhat, double* out) {
-  if ((size_t)s->nc * sizeof(double) * kElemWarps > 48 * 1024) {
-    set_error("element kernel: nc too large");
+  if (s->Q > 256 || s->nc > 256) {
+    set_error("element kernel: Q and nc must be <= 256");
     return MH_E_UNSUPPORTED;
   }
   switch (mode) {

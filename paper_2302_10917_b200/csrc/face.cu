@@ -321,13 +321,13 @@ __global__ void face_factor_kernel(const double* __restrict__ Drm, double* __res
 }
 
 __global__ void transpose_batched_kernel(const double* __restrict__ in, double* __restrict__ out,
-                                         int rows, int cols) {
+                                         int rows, int cols, int64_t ostride) {
   // in: batch x rows x cols (row-major) -> out: batch x cols x rows
   __shared__ double tile[32][33];
   const int64_t b = blockIdx.z;
   const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
   const double* ib = in + b * (size_t)rows * cols;
-  double* ob = out + b * (size_t)rows * cols;
+  double* ob = out + b * ostride;
   for (int k = threadIdx.y; k < 32; k += blockDim.y) {
     const int r = r0 + k, c = c0 + threadIdx.x;
     if (r < rows && c < cols) tile[k][threadIdx.x] = ib[(size_t)r * cols + c];
@@ -361,15 +361,16 @@ FaceArgs make_args(mh_system* s, const double* in, double* out) {
 }  // namespace
 
 int launch_transpose_batched(cudaStream_t st, const double* in, double* out, int64_t batch,
-                             int rows, int cols) {
+                             int rows, int cols, int64_t ostride) {
   if (batch == 0) return MH_OK;
+  if (ostride < 0) ostride = (int64_t)rows * cols;
   dim3 grid((cols + 31) / 32, (rows + 31) / 32, 1);
   dim3 block(32, 8);
   for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
     const int64_t nb = batch - b0 < 65535 ? batch - b0 : 65535;
     grid.z = (unsigned)nb;
     transpose_batched_kernel<<<grid, block, 0, st>>>(in + b0 * (size_t)rows * cols,
-                                                     out + b0 * (size_t)rows * cols, rows, cols);
+                                                     out + b0 * ostride, rows, cols, ostride);
     MH_CHECK_CUDA(cudaGetLastError());
   }
   return MH_OK;

@@ -7,7 +7,8 @@
 // Pivot rule = LAPACK idamax (largest |a_ik|, first index on ties); the pivot
 // column is scaled by the reciprocal of the pivot when |pivot| >= DBL_MIN, as
 // dgetf2 does; a zero pivot skips the swap/scale (LAPACK info > 0 path).
-// Output layout (device): LU column-major packed L\U per block, 1/U_jj,
+// Output layout (device): per block the packed streams of the element kernel
+// (strict lower L by columns 0..Q-2, strict upper U by columns Q-1..1), diag(U), 1/U_jj,
 // LAPACK 0-based pivots, and the composed row permutation used by the
 // element kernel (x_perm[i] = x[perm[i]]).
 //
@@ -17,6 +18,7 @@
 //   * otherwise the block is factored in place in its HBM output slot
 //     (L2-resident working set), e.g. Q = 220 (387 KB).
 
+#include <algorithm>
 #include <cfloat>
 
 #include "mh_internal.h"
@@ -38,10 +40,37 @@ __device__ __forceinline__ double block_max(double v, double* red) {
   return r;
 }
 
-__global__ void __launch_bounds__(kLuThreads)
-lu_kernel(const double* __restrict__ A, double* __restrict__ LU, double* __restrict__ dinv,
-          int32_t* __restrict__ piv, int32_t* __restrict__ perm, int32_t* __restrict__ stat,
-          int Q, int use_smem) {
+struct LuArgs {
+  const double* A;   // N x Q x Q row-major input
+  double* LU;        // workspace (global variant only)
+  double* Lp;        // N x ldL packed strict lower, columns 0..Q-2
+  double* Up;        // N x ldL packed strict upper, columns Q-1..1
+  double* udiag;     // N x Q
+  double* dinv;      // N x Q
+  int32_t* piv;      // N x Q
+  int32_t* perm;     // N x Q
+  int32_t* stat;     // N
+  int64_t ldL;
+  int Q;
+  int use_smem;
+};
+
+// packed-layout offsets (see element.cu)
+__host__ __device__ __forceinline__ int64_t off_lower(int j, int Q) {
+  return (int64_t)j * (Q - 1) - (int64_t)j * (j - 1) / 2;
+}
+__host__ __device__ __forceinline__ int64_t off_upper(int j, int Q) {
+  return (int64_t)Q * (Q - 1) / 2 - (int64_t)j * (j + 1) / 2;
+}
+
+__global__ void __launch_bounds__(kLuThreads) lu_kernel(LuArgs g) {
+  const double* __restrict__ A = g.A;
+  double* __restrict__ LU = g.LU;
+  double* __restrict__ dinv = g.dinv;
+  int32_t* __restrict__ piv = g.piv;
+  int32_t* __restrict__ perm = g.perm;
+  int32_t* __restrict__ stat = g.stat;
+  const int Q = g.Q, use_smem = g.use_smem;
   extern __shared__ double smem[];
   __shared__ double red[kLuThreads / 32];
   __shared__ int s_perm[kLuMaxQ];
@@ -116,13 +145,26 @@ lu_kernel(const double* __restrict__ A, double* __restrict__ LU, double* __restr
     __syncthreads();
   }
 
-  // write back, reciprocal diagonal, permutation, singular flag
-  double* LUe = LU + e * QQ;
-  if (use_smem)
-    for (size_t idx = tid; idx < QQ; idx += kLuThreads) LUe[idx] = W[idx];
+  // write the packed streams (L columns ascending, U columns descending),
+  // diag(U), its reciprocal, the permutation and the singular flag
+  double* Lpe = g.Lp + e * g.ldL;
+  double* Upe = g.Up + e * g.ldL;
+  for (int j = warp; j < Q; j += NW) {
+    const double* cj = W + (size_t)j * Q;
+    const int64_t ol = off_lower(j, Q), ou = off_upper(j, Q);
+    for (int i = lane; i < Q; i += 32) {
+      if (i > j) Lpe[ol + (i - j - 1)] = cj[i];
+      else if (i < j) Upe[ou + i] = cj[i];
+    }
+  }
+  if (tid == 0 && ((int64_t)Q * (Q - 1) / 2) < g.ldL) {  // zero the pad so it streams clean
+    Lpe[g.ldL - 1] = 0.0;
+    Upe[g.ldL - 1] = 0.0;
+  }
   double dmin = DBL_MAX;
   for (int i = tid; i < Q; i += kLuThreads) {
     const double d = W[(size_t)i * Q + i];
+    g.udiag[e * Q + i] = d;
     dinv[e * Q + i] = 1.0 / d;
     perm[e * Q + i] = s_perm[i];
     dmin = fmin(dmin, fabs(d));
@@ -137,7 +179,34 @@ lu_kernel(const double* __restrict__ A, double* __restrict__ LU, double* __restr
   }
 }
 
+__global__ void unpack_lu_kernel(const double* __restrict__ Lp, const double* __restrict__ Up,
+                                 const double* __restrict__ udiag, int64_t ldL, int Q,
+                                 int64_t first, int64_t count, double* __restrict__ out) {
+  const int64_t QQ = (int64_t)Q * Q;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < count * QQ;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = idx / QQ, e = first + b;
+    const int r = (int)(idx - b * QQ);
+    const int i = r / Q, j = r - i * Q;
+    double v;
+    if (i > j) v = Lp[e * ldL + off_lower(j, Q) + (i - j - 1)];
+    else if (i < j) v = Up[e * ldL + off_upper(j, Q) + i];
+    else v = udiag[e * Q + i];
+    out[idx] = v;
+  }
+}
+
 }  // namespace
+
+int launch_unpack_lu(mh_system* s, int64_t first, int64_t count, double* out) {
+  if (count <= 0) return MH_OK;
+  const int64_t total = count * (int64_t)s->Q * s->Q;
+  const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 65535);
+  unpack_lu_kernel<<<grid, 256, 0, s->stream>>>(s->Lp.p, s->Up.p, s->udiag.p, s->ldL, s->Q, first,
+                                                count, out);
+  MH_CHECK_CUDA(cudaGetLastError());
+  return MH_OK;
+}
 
 int launch_lu(mh_system* s, float* ms) {
   if (s->Q > kLuMaxQ) {
@@ -161,8 +230,21 @@ int launch_lu(mh_system* s, float* ms) {
     MH_CHECK_CUDA(cudaEventCreate(&e1));
     MH_CHECK_CUDA(cudaEventRecord(e0, s->stream));
   }
-  lu_kernel<<<(unsigned)s->N, kLuThreads, dyn, s->stream>>>(
-      s->A.p, s->LU.p, s->dinv.p, s->piv.p, s->perm.p, s->lstat.p, s->Q, use_smem);
+  if (!use_smem) MH_CHECK(s->LU.alloc((size_t)s->N * s->Q * s->Q));
+  LuArgs g;
+  g.A = s->A.p;
+  g.LU = s->LU.p;
+  g.Lp = s->Lp.p;
+  g.Up = s->Up.p;
+  g.udiag = s->udiag.p;
+  g.dinv = s->dinv.p;
+  g.piv = s->piv.p;
+  g.perm = s->perm.p;
+  g.stat = s->lstat.p;
+  g.ldL = s->ldL;
+  g.Q = s->Q;
+  g.use_smem = use_smem;
+  lu_kernel<<<(unsigned)s->N, kLuThreads, dyn, s->stream>>>(g);
   MH_CHECK_CUDA(cudaGetLastError());
   if (ms) {
     MH_CHECK_CUDA(cudaEventRecord(e1, s->stream));

@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <cstddef>
+#include <utility>
 #include <string>
 #include <vector>
 
@@ -89,7 +90,12 @@ struct mh_system {
 
   // blocks
   mh::DBuf<double> A;      // staged A, N*Q*Q row-major (input of the LU)
-  mh::DBuf<double> LU;     // N*Q*Q column-major packed L\U
+  mh::DBuf<double> LU;     // N*Q*Q column-major workspace (only when Q*Q*8 > smem)
+  mh::DBuf<double> Lp;     // N*ldL packed strict lower L, columns 0..Q-2 (streamed)
+  mh::DBuf<double> Up;     // N*ldL packed strict upper U, columns Q-1..1 (streamed)
+  mh::DBuf<double> udiag;  // N*Q   diag(U)
+  int64_t ldB = 0;         // per-macro stride of Bt / Cm (nc*Q rounded up to even)
+  int64_t ldL = 0;         // per-macro stride of Lp / Up (Q(Q-1)/2 rounded up to even)
   mh::DBuf<double> dinv;   // N*Q   1/U_ii
   mh::DBuf<int32_t> piv;   // N*Q   LAPACK 0-based pivots
   mh::DBuf<int32_t> perm;  // N*Q   composed row permutation: (P x)_i = x[perm_i]
@@ -113,6 +119,11 @@ struct mh_system {
 
   mh::Krylov* kry = nullptr;
 
+  // optional per-kernel event timing (mh_profile)
+  bool profiling = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_elem, ev_face;
+
   // multi-GPU
   int nranks = 1, rank = 0;
   void* nccl = nullptr;  // ncclComm_t
@@ -131,9 +142,13 @@ int launch_face_factor(mh_system* s, const double* Drm);
 int launch_face_reduce(mh_system* s, const double* uhat, double* w, int rhs_mode, int fuse_precond);
 int launch_precond(mh_system* s, const double* w, double* z);
 int launch_transpose_batched(cudaStream_t st, const double* in, double* out, int64_t batch,
-                             int rows, int cols);
+                             int rows, int cols, int64_t out_stride = -1);
+int launch_unpack_lu(mh_system* s, int64_t first, int64_t count, double* out_rowmajor);
 // krylov.cu
 void free_krylov(Krylov* k);
+// capi.cu: event-timed launch brackets (no-ops unless profiling)
+int prof_begin(mh_system* s, cudaEvent_t* ev);
+int prof_end(mh_system* s, cudaEvent_t ev0, int kind);  // kind 0 element, 1 face
 // comm.cu (multi-GPU halo; no-ops on a single device)
 int halo_u_exchange(mh_system* s, const double* u, const double** u_halo);
 int halo_v_exchange(mh_system* s);
