@@ -212,9 +212,10 @@ extern "C" int mh_upload_connectivity(mh_system* s, const int32_t* elem_ufac,
 
 static int alloc_blocks(mh_system* s) {
   const size_t N = (size_t)s->N, Q = s->Q, nc = s->nc, F = (size_t)s->F, t = s->t;
-  s->ldB = ((int64_t)nc * Q + 1) & ~(int64_t)1;
-  s->ldL = ((int64_t)Q * (Q - 1) / 2 + 1) & ~(int64_t)1;
-  if (s->ldL < 2) s->ldL = 2;
+  const int64_t ch = kStreamChunk;
+  s->ldB = ((int64_t)nc * Q + ch - 1) / ch * ch;
+  s->ldL = ((int64_t)Q * (Q - 1) / 2 + ch - 1) / ch * ch;
+  if (s->ldL < ch) s->ldL = ch;
   MH_CHECK(s->A.alloc(N * Q * Q));
   MH_CHECK(s->Lp.alloc(N * (size_t)s->ldL));
   MH_CHECK(s->Up.alloc(N * (size_t)s->ldL));
@@ -256,7 +257,7 @@ static int upload_impl(mh_system* s, const double* A, const double* B, const dou
   if (!s->c_is_bt) MH_CHECK(s->Cm.alloc(N * (size_t)s->ldB));
   else s->Cm.release();
   const size_t row = sizeof(double) * nc * Q, pitch = sizeof(double) * (size_t)s->ldB;
-  if (N && (s->ldB & 1) == 0 && (size_t)s->ldB != nc * Q)  // zero the per-macro pad
+  if (N && (size_t)s->ldB != nc * Q)  // zero the per-macro pad (streamed, never used)
     MH_CHECK_CUDA(cudaMemsetAsync(s->Bt.p, 0, pitch * N, st));
   if (B == nullptr) {
     if (N) MH_CHECK_CUDA(cudaMemcpy2DAsync(s->Bt.p, pitch, C, row, row, N, kind, st));

@@ -34,9 +34,9 @@
 namespace mh {
 namespace {
 
-constexpr int kWPB = 4;        // warps (pipelines) per CTA
-constexpr int kRingD = 2048;   // doubles per warp ring (16 KB)
-constexpr int kChunk = 256;    // doubles per bulk-copy chunk (2 KB)
+constexpr int kWPB = 4;                 // warps (pipelines) per CTA
+constexpr int kRingD = 2048;            // doubles per warp ring (16 KB)
+constexpr int kChunk = kStreamChunk;    // doubles per bulk-copy chunk (4 KB)
 using RingT = Ring<kRingD, kChunk>;
 constexpr uint32_t kM = RingT::M;
 
@@ -176,18 +176,17 @@ element_kernel(ElemArgs a) {
   __shared__ RingState rst[kWPB];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int Q = a.Q, nc = a.nc, t = a.t;
-  const int lenB = (int)(((int64_t)nc * Q + 1) & ~1);
-  const int lenL = (int)(((int64_t)Q * (Q - 1) / 2 + 1) & ~1);
+  const int nchB = (int)(a.ldB / kChunk), nchL = (int)(a.ldL / kChunk);
   int nseg = 0;
   if (MODE != kRhs) ++nseg;
   nseg += 2;
   if (MODE != kRecon) ++nseg;
   if (threadIdx.x == 0) {
     int n = 0;
-    if (MODE != kRhs) segs[n++] = Segment{a.Bt, a.ldB, lenB, (MODE == kApply && a.c_is_bt) ? 1 : 0};
-    segs[n++] = Segment{a.Lp, a.ldL, lenL, 0};
-    segs[n++] = Segment{a.Up, a.ldL, lenL, 0};
-    if (MODE != kRecon) segs[n++] = Segment{a.Cm, a.ldB, lenB, 0};
+    if (MODE != kRhs) segs[n++] = Segment{a.Bt, a.ldB, nchB, (MODE == kApply && a.c_is_bt) ? 1 : 0};
+    segs[n++] = Segment{a.Lp, a.ldL, nchL, 0};
+    segs[n++] = Segment{a.Up, a.ldL, nchL, 0};
+    if (MODE != kRecon) segs[n++] = Segment{a.Cm, a.ldB, nchB, 0};
   }
   __syncthreads();  // the only CTA-wide barrier
   double* ring = reinterpret_cast<double*>(smem_raw) + (size_t)w * kRingD;
@@ -199,12 +198,12 @@ element_kernel(ElemArgs a) {
 
   const int64_t gw = (int64_t)blockIdx.x * kWPB + w;
   const int64_t W = (int64_t)gridDim.x * kWPB;
-  const uint32_t offL = (MODE != kRhs) ? (uint32_t)lenB : 0u;
-  const uint32_t offU = offL + (uint32_t)lenL;
-  const uint32_t offC = offU + (uint32_t)lenL;
-  const uint32_t E = offC + ((MODE != kRecon) ? (uint32_t)lenB : 0u);
+  const uint32_t offL = (MODE != kRhs) ? (uint32_t)a.ldB : 0u;
+  const uint32_t offU = offL + (uint32_t)a.ldL;
+  const uint32_t offC = offU + (uint32_t)a.ldL;
+  const uint32_t E = offC + ((MODE != kRecon) ? (uint32_t)a.ldB : 0u);
   RingState* st = &rst[w];
-  RingT::init(st, lane, ring, bars, segs, nseg, gw, W, a.N, E);
+  RingT::init(st, lane, ring, bars, segs, nseg, gw, W, a.N);
   uint32_t ready = 0;
 #define MH_WINDOW(A_, B_) \
   if ((B_) > ready) ready = RingT::slow(st, (A_), (B_), lane)

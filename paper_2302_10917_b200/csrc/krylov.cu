@@ -216,7 +216,6 @@ int gmres_core(cudaStream_t st, Krylov* K, int64_t n, const OpFn& A, const OpFn&
   auto Hat = [&](int i, int k) -> double& { return H[(size_t)i * m + k]; };
   double* V = K->V.p;
   const dim3 vg(kVecGrid), vb(kVecThreads);
-  bool breakdown_exit = false;
   while (it < maxiter && !conv) {
     // r = M(b - A x)
     MH_CHECK(A(x, K->tmp.p));
@@ -302,12 +301,8 @@ int gmres_core(cudaStream_t st, Krylov* K, int64_t n, const OpFn& A, const OpFn&
       MH_CHECK_CUDA(cudaGetLastError());
       MH_CHECK_CUDA(cudaStreamSynchronize(st));  // h_host reused below
     }
-    if (breakdown && !conv) {
-      breakdown_exit = true;
-      break;
-    }
+    if (breakdown && !conv) break;  // invariant Krylov subspace
   }
-  (void)breakdown_exit;
   if (!conv) {  // one true-residual recheck (schur_solver.py:382-384)
     MH_CHECK(A(x, K->tmp.p));
     sub_kernel<<<vg, vb, 0, st>>>(n, rhs, K->tmp.p, K->tmp2.p);

@@ -157,9 +157,9 @@ __global__ void __launch_bounds__(kLuThreads) lu_kernel(LuArgs g) {
       else if (i < j) Upe[ou + i] = cj[i];
     }
   }
-  if (tid == 0 && ((int64_t)Q * (Q - 1) / 2) < g.ldL) {  // zero the pad so it streams clean
-    Lpe[g.ldL - 1] = 0.0;
-    Upe[g.ldL - 1] = 0.0;
+  for (int64_t i = (int64_t)Q * (Q - 1) / 2 + tid; i < g.ldL; i += kLuThreads) {
+    Lpe[i] = 0.0;  // zero the pad so it streams clean
+    Upe[i] = 0.0;
   }
   double dmin = DBL_MAX;
   for (int i = tid; i < Q; i += kLuThreads) {

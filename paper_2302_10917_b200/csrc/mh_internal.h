@@ -35,6 +35,9 @@ constexpr unsigned kFull = 0xffffffffu;
 // fixed reduction partition: results never depend on the device or SM count
 constexpr int kDotBlocks = 512;
 constexpr int kDotThreads = 256;
+// chunk (doubles) of the element kernel's bulk-copy stream; the per-macro
+// strides of the streamed arrays (op.B^T, L, U, op.C) are multiples of it
+constexpr int kStreamChunk = 512;
 
 // Device buffer with RAII-less explicit free (the system owns them).
 template <class T>
@@ -94,8 +97,8 @@ struct mh_system {
   mh::DBuf<double> Lp;     // N*ldL packed strict lower L, columns 0..Q-2 (streamed)
   mh::DBuf<double> Up;     // N*ldL packed strict upper U, columns Q-1..1 (streamed)
   mh::DBuf<double> udiag;  // N*Q   diag(U)
-  int64_t ldB = 0;         // per-macro stride of Bt / Cm (nc*Q rounded up to even)
-  int64_t ldL = 0;         // per-macro stride of Lp / Up (Q(Q-1)/2 rounded up to even)
+  int64_t ldB = 0;         // per-macro stride of Bt / Cm (nc*Q rounded up to kStreamChunk)
+  int64_t ldL = 0;         // per-macro stride of Lp / Up (Q(Q-1)/2 rounded up to kStreamChunk)
   mh::DBuf<double> dinv;   // N*Q   1/U_ii
   mh::DBuf<int32_t> piv;   // N*Q   LAPACK 0-based pivots
   mh::DBuf<int32_t> perm;  // N*Q   composed row permutation: (P x)_i = x[perm_i]

@@ -7,9 +7,9 @@
 //
 // Stream positions are 32-bit (doubles).  The stream of a warp is the
 // concatenation, over the macros it owns (e = e0, e0 + W, e0 + 2W, ...),
-// of up to 4 per-macro segments (e.g. op.B^T | L | U | op.C).  Segment
-// lengths and per-macro strides are even, so every copy is 16-byte aligned
-// and a multiple of 16 bytes, as cp.async.bulk requires.
+// of up to 4 per-macro segments (e.g. op.B^T | L | U | op.C), each padded
+// in HBM to whole chunks, so chunk c of the stream is one bulk copy into
+// ring slot c % S.
 //
 // Consumer protocol (warp-uniform): before reading stream positions
 // [a, b) call `window(a, b)`; it is a single compare on the fast path.  On
@@ -68,27 +68,28 @@ __device__ __forceinline__ uint64_t l2_policy_evict_last() {
   return p;
 }
 
+// Per-macro segment of the stream.  Every segment is padded to a multiple
+// of the chunk size CH in HBM, so each chunk is exactly one bulk copy.
 struct Segment {
   const double* base;  // segment of macro e starts at base + e * stride
-  int64_t stride;      // doubles between consecutive macros (even)
-  int len;             // doubles in the segment (even)
+  int64_t stride;      // doubles between consecutive macros (multiple of CH)
+  int nch;             // chunks in the segment
   int keep;            // 1: L2 evict_last (re-read soon), 0: evict_first
 };
 
 // Ring state of one warp, kept in shared memory so that the out-of-line
 // slow path does not force the consumer's registers onto the stack.
 struct RingState {
-  const Segment* seg;
+  Segment seg[4];
   double* ring;
   uint64_t* bar;
-  int64_t pe;          // producer cursor: macro of the next copy
+  int64_t pe;          // producer cursor: macro of the next chunk
   int64_t W;           // macro stride between a warp's macros
   uint64_t pol_first, pol_last;
-  uint32_t total;      // stream length (doubles)
+  uint32_t nchunks;    // chunks in this warp's stream
   uint32_t issued;     // chunks issued
   uint32_t waited;     // chunks landed
-  uint32_t po;         // producer cursor: offset in segment
-  int ps;              // producer cursor: segment
+  int ps, pq;          // producer cursor: segment, chunk within segment
   int nseg;
 };
 
@@ -99,12 +100,15 @@ struct Ring {
   static_assert((RING & (RING - 1)) == 0, "ring must be a power of two");
   static_assert(RING % CH == 0 && S >= 2, "ring must hold >= 2 chunks");
 
-  // E = doubles per macro; returns the stream length of this warp
   static __device__ void init(RingState* st, int lane, double* ring, uint64_t* bar,
                               const Segment* seg, int nseg, int64_t e0, int64_t W,
-                              int64_t nmacro, uint32_t E) {
+                              int64_t nmacro) {
     if (lane == 0) {
-      st->seg = seg;
+      int per = 0;
+      for (int s = 0; s < nseg; ++s) {
+        st->seg[s] = seg[s];
+        per += seg[s].nch;
+      }
       st->ring = ring;
       st->bar = bar;
       st->pe = e0;
@@ -112,62 +116,51 @@ struct Ring {
       st->pol_first = l2_policy_evict_first();
       st->pol_last = l2_policy_evict_last();
       const int64_t mine = e0 < nmacro ? (nmacro - e0 + W - 1) / W : 0;
-      st->total = (uint32_t)(mine * (int64_t)E);
+      st->nchunks = (uint32_t)(mine * per);
       st->issued = st->waited = 0;
-      st->po = 0;
       st->ps = 0;
+      st->pq = 0;
       st->nseg = nseg;
+      while (st->seg[st->ps].nch == 0) ++st->ps;  // skip empty leading segments
       for (int i = 0; i < S; ++i) mbar_init(&bar[i], 1);
       fence_mbar_init();
     }
     __syncwarp();
   }
 
-  // lane 0: issue chunk c (copies covering stream positions [c*CH, c*CH+CH))
-  static __device__ void issue_chunk(RingState* st, uint32_t c) {
+  // lane 0: issue the next chunk (one 8*CH-byte bulk copy)
+  static __device__ __forceinline__ void issue_next(RingState* st, uint32_t c) {
     const int slot = (int)(c % S);
-    const uint32_t p0 = c * CH;
-    const uint32_t p1 = min(p0 + (uint32_t)CH, st->total);
-    mbar_expect_tx(&st->bar[slot], (p1 - p0) * 8u);
-    uint32_t p = p0;
-    uint32_t po = st->po;
-    int ps = st->ps;
-    int64_t pe = st->pe;
-    const Segment* seg = st->seg;
-    while (p < p1) {
-      while (po >= (uint32_t)seg[ps].len) {  // skip finished / empty segments
-        po = 0;
-        if (++ps == st->nseg) {
-          ps = 0;
-          pe += st->W;
+    const Segment& sg = st->seg[st->ps];
+    mbar_expect_tx(&st->bar[slot], CH * 8u);
+    bulk_g2s(st->ring + slot * CH, sg.base + st->pe * sg.stride + (int64_t)st->pq * CH, CH * 8u,
+             &st->bar[slot], sg.keep ? st->pol_last : st->pol_first);
+    if (++st->pq == sg.nch) {
+      st->pq = 0;
+      do {
+        if (++st->ps == st->nseg) {
+          st->ps = 0;
+          st->pe += st->W;
         }
-      }
-      const uint32_t len = min(p1 - p, (uint32_t)seg[ps].len - po);
-      bulk_g2s(st->ring + (p & M), seg[ps].base + pe * seg[ps].stride + po, len * 8u,
-               &st->bar[slot], seg[ps].keep ? st->pol_last : st->pol_first);
-      p += len;
-      po += len;
+      } while (st->seg[st->ps].nch == 0);
     }
-    st->po = po;
-    st->ps = ps;
-    st->pe = pe;
   }
 
-  // Slow path of window(): release [.., a), refill, wait for [.., b).
-  // Returns the new ready end (stream position up to which data landed).
+  // Slow path of the consumer's window check: release [.., a), refill,
+  // wait for [.., b).  Returns the new ready end (stream position up to
+  // which data has landed).
   static __device__ __noinline__ uint32_t slow(RingState* st, uint32_t a, uint32_t b, int lane) {
-    const uint32_t total = st->total;
-    const uint32_t nchunks = (total + CH - 1) / CH;
     uint32_t limit = a / CH + S;
+    const uint32_t nchunks = st->nchunks;
     if (limit > nchunks) limit = nchunks;
     const uint32_t issued = st->issued;
+    uint32_t waited = st->waited;
     __syncwarp();  // every lane is done with the slots being refilled
-    if (issued < limit && lane == 0) {
+    if (lane == 0 && issued < limit) {
       fence_proxy_async_smem();
-      for (uint32_t c = issued; c < limit; ++c) issue_chunk(st, c);
+      for (uint32_t c = issued; c < limit; ++c) issue_next(st, c);
       st->issued = limit;
     }
-    uint32_t waited = st->waited;
     while (waited * CH < b) {
       const int slot = (int)(waited % S);
       const uint32_t parity = (waited / S) & 1u;
@@ -177,7 +170,6 @@ struct Ring {
     }
     __syncwarp();
     if (lane == 0) st->waited = waited;
-    __syncwarp();
     return waited * CH;
   }
 };
