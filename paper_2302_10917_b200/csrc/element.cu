@@ -34,11 +34,14 @@
 namespace mh {
 namespace {
 
-constexpr int kWPB = 4;                 // warps (pipelines) per CTA
-constexpr int kRingD = 2048;            // doubles per warp ring (16 KB)
+constexpr int kWPB = 4;                 // consumer warps (macros in flight) per CTA
+constexpr int kThreads = (kWPB + 1) * 32;  // + one producer warp
+constexpr int kRingD = 2048;            // doubles per consumer ring (16 KB)
 constexpr int kChunk = kStreamChunk;    // doubles per bulk-copy chunk (4 KB)
-using RingT = Ring<kRingD, kChunk>;
-constexpr uint32_t kM = RingT::M;
+constexpr int kS = kRingD / kChunk;
+using PipeT = Pipe<kRingD, kChunk, kWPB>;
+using ConsT = Consumer<kRingD, kChunk>;
+constexpr uint32_t kM = kRingD - 1;
 
 struct ElemArgs {
   const int32_t* elem_ufac;
@@ -77,139 +80,124 @@ __device__ __forceinline__ bool no_wrap(uint32_t lo, uint32_t span) {
   return (lo & kM) + span <= (uint32_t)kRingD;
 }
 
-// x_i += sum over 4 rows c of op.B^T[c][perm_i] * ue_c, rows at stream p, p+Q, ...
-template <int R, bool WRAP, bool PERM>
-__device__ __forceinline__ void gemv_rows4(double (&acc)[R], const double* ring, uint32_t p,
-                                           int nrow, int Q, const double* su, const int (&pr)[R],
-                                           int lane) {
+// x_i += sum over NR rows c of op.B^T[c][perm_i] * ue_c, rows at stream p, p+Q, ...
+template <int R, int NR, bool WRAP, bool PERM>
+__device__ __forceinline__ void gemv_rows(double (&acc)[R], const double* ring, uint32_t p, int Q,
+                                          const double* su, const int (&pr)[R], int lane) {
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    if (u < nrow) {
-      const double uc = su[u];
-      const double* cb = ring + (p & kM);
+  for (int u = 0; u < NR; ++u) {
+    const double uc = su[u];
+    const double* cb = ring + (p & kM);
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int i = PERM ? pr[r] : lane + 32 * r;
-        const double b = WRAP ? ring[(p + (uint32_t)i) & kM] : cb[i];
-        if (lane + 32 * r < Q) acc[r] = fma(b, uc, acc[r]);
-      }
-      p += Q;
+    for (int r = 0; r < R; ++r) {
+      const int i = PERM ? pr[r] : lane + 32 * r;
+      const double b = WRAP ? ring[(p + (uint32_t)i) & kM] : cb[i];
+      if (lane + 32 * r < Q) acc[r] = fma(b, uc, acc[r]);
     }
+    p += Q;
   }
 }
 
-// forward substitution over 4 packed L columns j0..j0+3 (JB = j0 / 32 is a
+// forward substitution over NC packed L columns j0.. (JB = j0 / 32 is a
 // compile-time constant once the caller's block loop is unrolled)
-template <int R, bool WRAP>
-__device__ __forceinline__ void fwd_cols4(double (&y)[R], const double* ring, uint32_t p, int JB,
-                                          int j0, int Q, int lane) {
+template <int R, int NC, bool WRAP>
+__device__ __forceinline__ void fwd_cols(double (&y)[R], const double* ring, uint32_t p, int JB,
+                                         int j0, int Q, int lane) {
   const int jj0 = j0 & 31;
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
+  for (int u = 0; u < NC; ++u) {
     const int j = j0 + u;
-    if (j < Q - 1) {
-      const uint32_t q0 = p - (uint32_t)(j + 1);  // stream position of "row 0"
-      const double yj = __shfl_sync(kFull, y[JB], jj0 + u);
-      const double* cb = ring + (q0 & kM);
+    const uint32_t q0 = p - (uint32_t)(j + 1);  // stream position of "row 0"
+    const double yj = __shfl_sync(kFull, y[JB], jj0 + u);
+    const double* cb = ring + (q0 & kM);
 #pragma unroll
-      for (int r = JB; r < R; ++r) {
-        const int i = lane + 32 * r;
-        const double l = WRAP ? ring[(q0 + (uint32_t)i) & kM] : cb[i];
-        if (r > JB || lane > jj0 + u) y[r] = fma(-l, yj, y[r]);
-      }
-      p += (uint32_t)(Q - 1 - j);
+    for (int r = JB; r < R; ++r) {
+      const int i = lane + 32 * r;
+      const double l = WRAP ? ring[(q0 + (uint32_t)i) & kM] : cb[i];
+      if (r > JB || lane > jj0 + u) y[r] = fma(-l, yj, y[r]);
     }
+    p += (uint32_t)(Q - 1 - j);
   }
 }
 
-// back substitution over 4 packed U columns j0, j0-1, .. (descending; JB = j0 / 32)
-template <int R, bool WRAP>
-__device__ __forceinline__ void bwd_cols4(double (&y)[R], const double (&dr)[R],
-                                          const double* ring, uint32_t p, int JB, int j0,
-                                          int lane) {
+// back substitution over NC packed U columns j0, j0-1, .. (descending)
+template <int R, int NC, bool WRAP>
+__device__ __forceinline__ void bwd_cols(double (&y)[R], const double (&dr)[R],
+                                         const double* ring, uint32_t p, int JB, int j0,
+                                         int lane) {
   const int jj0 = j0 & 31;
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
+  for (int u = 0; u < NC; ++u) {
     const int j = j0 - u;
-    if (j >= JB * 32) {
-      if (lane == jj0 - u) y[JB] *= dr[JB];
-      const double yj = __shfl_sync(kFull, y[JB], jj0 - u);
-      const double* cb = ring + (p & kM);
+    if (lane == jj0 - u) y[JB] *= dr[JB];
+    const double yj = __shfl_sync(kFull, y[JB], jj0 - u);
+    const double* cb = ring + (p & kM);
 #pragma unroll
-      for (int r = 0; r <= JB; ++r) {
-        const int i = lane + 32 * r;
-        const double uv = WRAP ? ring[(p + (uint32_t)i) & kM] : cb[i];
-        if (r < JB || lane < jj0 - u) y[r] = fma(-uv, yj, y[r]);
-      }
-      p += (uint32_t)j;
+    for (int r = 0; r <= JB; ++r) {
+      const int i = lane + 32 * r;
+      const double uv = WRAP ? ring[(p + (uint32_t)i) & kM] : cb[i];
+      if (r < JB || lane < jj0 - u) y[r] = fma(-uv, yj, y[r]);
     }
+    p += (uint32_t)j;
   }
 }
 
-// partial dot products of 4 op.C rows with y (rows at p, p+Q, ...) into pp[Q0..Q0+3]
+// partial dot product of one op.C row with y
 template <int R, bool WRAP>
-__device__ __forceinline__ void dot_rows4(double (&pp)[32], int Q0, const double (&y)[R],
-                                          const double* ring, uint32_t p, int nrow, int Q,
-                                          int lane) {
+__device__ __forceinline__ double dot_row(const double (&y)[R], const double* ring, uint32_t p,
+                                          int Q, int lane) {
+  double acc = 0.0;
+  const double* cb = ring + (p & kM);
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    double acc = 0.0;
-    if (u < nrow) {
-      const double* cb = ring + (p & kM);
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int i = lane + 32 * r;
-        const double c = WRAP ? ring[(p + (uint32_t)i) & kM] : cb[i];
-        if (i < Q) acc = fma(c, y[r], acc);
-      }
-      p += Q;
-    }
-    pp[Q0 + u] = acc;
+  for (int r = 0; r < R; ++r) {
+    const int i = lane + 32 * r;
+    const double c = WRAP ? ring[(p + (uint32_t)i) & kM] : cb[i];
+    if (i < Q) acc = fma(c, y[r], acc);
   }
+  return acc;
 }
 
 template <int R, int MODE>
-__global__ void __launch_bounds__(kWPB * 32, 3)
+__global__ void __launch_bounds__(kThreads, 3)
 element_kernel(ElemArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ Segment segs[4];
-  __shared__ RingState rst[kWPB];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int Q = a.Q, nc = a.nc, t = a.t;
   const int nchB = (int)(a.ldB / kChunk), nchL = (int)(a.ldL / kChunk);
-  int nseg = 0;
-  if (MODE != kRhs) ++nseg;
-  nseg += 2;
-  if (MODE != kRecon) ++nseg;
+  double* rings = reinterpret_cast<double*>(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(rings + (size_t)kWPB * kRingD);
+  uint64_t* empty = full + kWPB * kS;
+  double* su_all = reinterpret_cast<double*>(empty + kWPB * kS);
+  const int nseg = (MODE != kRhs ? 1 : 0) + 2 + (MODE != kRecon ? 1 : 0);
   if (threadIdx.x == 0) {
     int n = 0;
     if (MODE != kRhs) segs[n++] = Segment{a.Bt, a.ldB, nchB, (MODE == kApply && a.c_is_bt) ? 1 : 0};
     segs[n++] = Segment{a.Lp, a.ldL, nchL, 0};
     segs[n++] = Segment{a.Up, a.ldL, nchL, 0};
     if (MODE != kRecon) segs[n++] = Segment{a.Cm, a.ldB, nchB, 0};
+    for (int i = 0; i < 2 * kWPB * kS; ++i) mbar_init(&full[i], 1);  // full + empty
+    fence_mbar_init();
   }
   __syncthreads();  // the only CTA-wide barrier
-  double* ring = reinterpret_cast<double*>(smem_raw) + (size_t)w * kRingD;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<double*>(smem_raw) +
-                                               (size_t)kWPB * kRingD) + w * RingT::S;
-  double* su = reinterpret_cast<double*>(reinterpret_cast<uint64_t*>(
-                   reinterpret_cast<double*>(smem_raw) + (size_t)kWPB * kRingD) +
-               kWPB * RingT::S) + (size_t)w * ((nc + 3) & ~3);
-
-  const int64_t gw = (int64_t)blockIdx.x * kWPB + w;
   const int64_t W = (int64_t)gridDim.x * kWPB;
+  if (w == kWPB) {  // producer warp
+    if (lane == 0)
+      PipeT::produce(rings, full, empty, segs, nseg, (int64_t)blockIdx.x * kWPB, W, a.N, kWPB);
+    return;
+  }
+  const double* ring = rings + (size_t)w * kRingD;
+  double* su = su_all + (size_t)w * ((nc + 3) & ~3);
+  ConsT cs;
+  cs.full = full + w * kS;
+  cs.empty = empty + w * kS;
   const uint32_t offL = (MODE != kRhs) ? (uint32_t)a.ldB : 0u;
   const uint32_t offU = offL + (uint32_t)a.ldL;
   const uint32_t offC = offU + (uint32_t)a.ldL;
   const uint32_t E = offC + ((MODE != kRecon) ? (uint32_t)a.ldB : 0u);
-  RingState* st = &rst[w];
-  RingT::init(st, lane, ring, bars, segs, nseg, gw, W, a.N);
-  uint32_t ready = 0;
-#define MH_WINDOW(A_, B_) \
-  if ((B_) > ready) ready = RingT::slow(st, (A_), (B_), lane)
 
   uint32_t base = 0;
-  for (int64_t e = gw; e < a.N; e += W, base += E) {
+  for (int64_t e = (int64_t)blockIdx.x * kWPB + w; e < a.N; e += W, base += E) {
     int pr[R];
     double dr[R];
     bool ident = true;
@@ -239,16 +227,19 @@ element_kernel(ElemArgs a) {
 #pragma unroll
       for (int r = 0; r < R; ++r) acc[r] = 0.0;
       uint32_t p = base;
-      for (int c = 0; c < nc; c += 4, p += 4u * (uint32_t)Q) {  // step 1: x = B ue
-        const int nrow = min(4, nc - c);
-        const uint32_t span = (uint32_t)(nrow * Q);
-        MH_WINDOW(p, p + span);
-        if (no_wrap(p, span + 32u * R)) {
-          if (has_perm) gemv_rows4<R, false, true>(acc, ring, p, nrow, Q, su + c, pr, lane);
-          else gemv_rows4<R, false, false>(acc, ring, p, nrow, Q, su + c, pr, lane);
+      int c = 0;
+      for (; c + 4 <= nc; c += 4, p += 4u * (uint32_t)Q) {  // step 1: x = B ue
+        cs.window(p, p + 4u * Q, lane);
+        if (no_wrap(p, 4u * Q + 32u * R)) {
+          if (has_perm) gemv_rows<R, 4, false, true>(acc, ring, p, Q, su + c, pr, lane);
+          else gemv_rows<R, 4, false, false>(acc, ring, p, Q, su + c, pr, lane);
         } else {
-          gemv_rows4<R, true, true>(acc, ring, p, nrow, Q, su + c, pr, lane);
+          gemv_rows<R, 4, true, true>(acc, ring, p, Q, su + c, pr, lane);
         }
+      }
+      for (; c < nc; ++c, p += (uint32_t)Q) {
+        cs.window(p, p + Q, lane);
+        gemv_rows<R, 1, true, true>(acc, ring, p, Q, su + c, pr, lane);
       }
       __syncwarp();  // su is rewritten by the next macro
 #pragma unroll
@@ -258,20 +249,26 @@ element_kernel(ElemArgs a) {
       }
     }
 
-    // step 2a: unit-lower forward substitution over packed L columns
+    // step 2a: unit-lower forward substitution over packed L columns 0..Q-2
     {
       uint32_t p = base + offL;
 #pragma unroll
       for (int jb = 0; jb < R; ++jb) {
         const int jend = min(jb * 32 + 32, Q - 1);
-        for (int j0 = jb * 32; j0 < jend; j0 += 4) {
-          const int ncol = min(4, jend - j0);
-          const uint32_t span = (uint32_t)(ncol * (Q - 1 - j0) - ncol * (ncol - 1) / 2);
-          MH_WINDOW(p, p + span);
+        int j0 = jb * 32;
+        for (; j0 + 4 <= jend; j0 += 4) {
+          const uint32_t span = (uint32_t)(4 * (Q - 1 - j0) - 6);
+          cs.window(p, p + span, lane);
           if (no_wrap(p - (uint32_t)(j0 + 1), span + (uint32_t)(j0 + 1) + 32u * R + 8u))
-            fwd_cols4<R, false>(y, ring, p, jb, j0, Q, lane);
+            fwd_cols<R, 4, false>(y, ring, p, jb, j0, Q, lane);
           else
-            fwd_cols4<R, true>(y, ring, p, jb, j0, Q, lane);
+            fwd_cols<R, 4, true>(y, ring, p, jb, j0, Q, lane);
+          p += span;
+        }
+        for (; j0 < jend; ++j0) {
+          const uint32_t span = (uint32_t)(Q - 1 - j0);
+          cs.window(p, p + span, lane);
+          fwd_cols<R, 1, true>(y, ring, p, jb, j0, Q, lane);
           p += span;
         }
       }
@@ -282,15 +279,20 @@ element_kernel(ElemArgs a) {
       uint32_t p = base + offU;
 #pragma unroll
       for (int jb = R - 1; jb >= 0; --jb) {
-        for (int j0 = min(jb * 32 + 31, Q - 1); j0 >= jb * 32; j0 -= 4) {
-          const int ncol = min(4, j0 - jb * 32 + 1);
-          const uint32_t span = (uint32_t)(ncol * j0 - ncol * (ncol - 1) / 2);
-          MH_WINDOW(p, p + span);
+        int j0 = min(jb * 32 + 31, Q - 1);
+        for (; j0 - 3 >= jb * 32; j0 -= 4) {
+          const uint32_t span = (uint32_t)(4 * j0 - 6);
+          cs.window(p, p + span, lane);
           if (no_wrap(p, span + 32u * R + 8u))
-            bwd_cols4<R, false>(y, dr, ring, p, jb, j0, lane);
+            bwd_cols<R, 4, false>(y, dr, ring, p, jb, j0, lane);
           else
-            bwd_cols4<R, true>(y, dr, ring, p, jb, j0, lane);
+            bwd_cols<R, 4, true>(y, dr, ring, p, jb, j0, lane);
           p += span;
+        }
+        for (; j0 >= jb * 32; --j0) {
+          cs.window(p, p + j0, lane);
+          bwd_cols<R, 1, true>(y, dr, ring, p, jb, j0, lane);
+          p += (uint32_t)j0;
         }
       }
     }
@@ -308,26 +310,40 @@ element_kernel(ElemArgs a) {
     uint32_t p = base + offC;
     for (int c0 = 0; c0 < nc; c0 += 32) {
       double pp[32];
+      const int nrow = min(32, nc - c0);
 #pragma unroll
       for (int q0 = 0; q0 < 32; q0 += 4) {
-        const int nrow = max(0, min(4, nc - c0 - q0));
-        const uint32_t span = (uint32_t)(nrow * Q);
-        if (nrow > 0) MH_WINDOW(p, p + span);
-        if (no_wrap(p, span + 32u * R))
-          dot_rows4<R, false>(pp, q0, y, ring, p, nrow, Q, lane);
-        else
-          dot_rows4<R, true>(pp, q0, y, ring, p, nrow, Q, lane);
-        p += span;
+        if (q0 + 4 <= nrow) {
+          cs.window(p, p + 4u * Q, lane);
+          if (no_wrap(p, 4u * Q + 32u * R)) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) pp[q0 + u] = dot_row<R, false>(y, ring, p + u * Q, Q, lane);
+          } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) pp[q0 + u] = dot_row<R, true>(y, ring, p + u * Q, Q, lane);
+          }
+          p += 4u * Q;
+        } else {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (q0 + u < nrow) {
+              cs.window(p, p + Q, lane);
+              pp[q0 + u] = dot_row<R, true>(y, ring, p, Q, lane);
+              p += Q;
+            } else {
+              pp[q0 + u] = 0.0;
+            }
+          }
+        }
       }
       const double v = transpose_reduce32(pp, lane);
       if (c0 + lane < nc) a.out[e * nc + c0 + lane] = v;
     }
   }
-#undef MH_WINDOW
 }
 
 size_t smem_bytes(int nc) {
-  return (size_t)kWPB * kRingD * sizeof(double) + (size_t)kWPB * RingT::S * sizeof(uint64_t) +
+  return (size_t)kWPB * kRingD * sizeof(double) + (size_t)2 * kWPB * kS * sizeof(uint64_t) +
          (size_t)kWPB * ((nc + 3) & ~3) * sizeof(double);
 }
 
@@ -337,12 +353,12 @@ int launch_rm(mh_system* s, const ElemArgs& a) {
   auto kern = element_kernel<R, MODE>;
   MH_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
-  MH_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWPB * 32, smem));
+  MH_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
   if (per_sm < 1) per_sm = 1;
   int64_t grid = (int64_t)s->num_sms * per_sm;
   const int64_t need = (s->N + kWPB - 1) / kWPB;
   if (grid > need) grid = need;
-  kern<<<(unsigned)grid, kWPB * 32, smem, s->stream>>>(a);
+  kern<<<(unsigned)grid, kThreads, smem, s->stream>>>(a);
   MH_CHECK_CUDA(cudaGetLastError());
   return MH_OK;
 }

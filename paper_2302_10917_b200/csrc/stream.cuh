@@ -1,9 +1,10 @@
-// Per-warp TMA bulk-copy stream: a warp consumes a long sequence of
-// contiguous HBM segments through a shared-memory ring that its lane 0
-// keeps full with cp.async.bulk (the 1-D TMA engine) and mbarrier
-// completion.  Memory-level parallelism therefore does not depend on
-// registers or on the compiler hoisting loads: up to S chunks of CH
-// doubles are in flight per warp at all times.
+// Per-warp TMA bulk-copy stream: a consumer warp reads a long sequence of
+// contiguous HBM segments through a shared-memory ring that a producer warp
+// of the same CTA keeps full with cp.async.bulk (the 1-D TMA engine) and
+// mbarrier completion.  Memory-level parallelism therefore does not depend
+// on registers or on the compiler hoisting loads: up to S chunks of CH
+// doubles are in flight per consumer at all times, and the consumer's own
+// issue slots are spent on arithmetic.
 //
 // Stream positions are 32-bit (doubles).  The stream of a warp is the
 // concatenation, over the macros it owns (e = e0, e0 + W, e0 + 2W, ...),
@@ -13,9 +14,9 @@
 //
 // Consumer protocol (warp-uniform): before reading stream positions
 // [a, b) call `window(a, b)`; it is a single compare on the fast path.  On
-// the slow path it releases every chunk ending at or before `a`, refills
-// the ring and waits for the chunks covering [.., b).  b - a must not
-// exceed (S - 1) * CH.
+// the slow path it releases every chunk ending at or before `a` (empty
+// barrier arrive) and waits for the chunks covering [.., b) (full barrier
+// wait).  b - a must not exceed (S - 1) * CH.
 #pragma once
 
 #include <stdint.h>
@@ -68,6 +69,20 @@ __device__ __forceinline__ uint64_t l2_policy_evict_last() {
   return p;
 }
 
+__device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 // Per-macro segment of the stream.  Every segment is padded to a multiple
 // of the chunk size CH in HBM, so each chunk is exactly one bulk copy.
 struct Segment {
@@ -77,100 +92,100 @@ struct Segment {
   int keep;            // 1: L2 evict_last (re-read soon), 0: evict_first
 };
 
-// Ring state of one warp, kept in shared memory so that the out-of-line
-// slow path does not force the consumer's registers onto the stack.
-struct RingState {
-  Segment seg[4];
-  double* ring;
-  uint64_t* bar;
-  int64_t pe;          // producer cursor: macro of the next chunk
-  int64_t W;           // macro stride between a warp's macros
-  uint64_t pol_first, pol_last;
-  uint32_t nchunks;    // chunks in this warp's stream
-  uint32_t issued;     // chunks issued
-  uint32_t waited;     // chunks landed
-  int ps, pq;          // producer cursor: segment, chunk within segment
-  int nseg;
-};
-
-template <int RING, int CH>
-struct Ring {
+// Warp-specialised ring pipeline: a producer warp of the CTA owns the
+// streams of the CTA's consumer warps.  Per consumer ring of S slots:
+//   full[slot]   producer arrive.expect_tx + bulk copy complete_tx; consumer waits
+//   empty[slot]  consumer lane 0 arrives after the warp has read the slot;
+//                producer waits before refilling it
+template <int RING, int CH, int NCONS>
+struct Pipe {
   static constexpr int S = RING / CH;
   static constexpr uint32_t M = RING - 1;
   static_assert((RING & (RING - 1)) == 0, "ring must be a power of two");
   static_assert(RING % CH == 0 && S >= 2, "ring must hold >= 2 chunks");
 
-  static __device__ void init(RingState* st, int lane, double* ring, uint64_t* bar,
-                              const Segment* seg, int nseg, int64_t e0, int64_t W,
-                              int64_t nmacro) {
-    if (lane == 0) {
-      int per = 0;
-      for (int s = 0; s < nseg; ++s) {
-        st->seg[s] = seg[s];
-        per += seg[s].nch;
-      }
-      st->ring = ring;
-      st->bar = bar;
-      st->pe = e0;
-      st->W = W;
-      st->pol_first = l2_policy_evict_first();
-      st->pol_last = l2_policy_evict_last();
-      const int64_t mine = e0 < nmacro ? (nmacro - e0 + W - 1) / W : 0;
-      st->nchunks = (uint32_t)(mine * per);
-      st->issued = st->waited = 0;
-      st->ps = 0;
-      st->pq = 0;
-      st->nseg = nseg;
-      while (st->seg[st->ps].nch == 0) ++st->ps;  // skip empty leading segments
-      for (int i = 0; i < S; ++i) mbar_init(&bar[i], 1);
-      fence_mbar_init();
+  // producer warp, lane 0: feed the NCONS consumer streams until done
+  static __device__ void produce(double* rings, uint64_t* full, uint64_t* empty,
+                                 const Segment* seg, int nseg, int64_t warp0, int64_t W,
+                                 int64_t nmacro, int ncons) {
+    const uint64_t pol_first = l2_policy_evict_first();
+    const uint64_t pol_last = l2_policy_evict_last();
+    int per = 0;
+    for (int s = 0; s < nseg; ++s) per += seg[s].nch;
+    int64_t pe[NCONS];
+    uint32_t issued[NCONS], nchunks[NCONS];
+    int ps[NCONS], pq[NCONS];
+    int first_seg = 0;
+    while (first_seg < nseg && seg[first_seg].nch == 0) ++first_seg;
+    for (int w = 0; w < NCONS; ++w) {
+      const int64_t e0 = warp0 + w;
+      const int64_t mine = (w < ncons && e0 < nmacro) ? (nmacro - e0 + W - 1) / W : 0;
+      pe[w] = e0;
+      issued[w] = 0;
+      nchunks[w] = (uint32_t)(mine * per);
+      ps[w] = first_seg;
+      pq[w] = 0;
     }
-    __syncwarp();
-  }
-
-  // lane 0: issue the next chunk (one 8*CH-byte bulk copy)
-  static __device__ __forceinline__ void issue_next(RingState* st, uint32_t c) {
-    const int slot = (int)(c % S);
-    const Segment& sg = st->seg[st->ps];
-    mbar_expect_tx(&st->bar[slot], CH * 8u);
-    bulk_g2s(st->ring + slot * CH, sg.base + st->pe * sg.stride + (int64_t)st->pq * CH, CH * 8u,
-             &st->bar[slot], sg.keep ? st->pol_last : st->pol_first);
-    if (++st->pq == sg.nch) {
-      st->pq = 0;
-      do {
-        if (++st->ps == st->nseg) {
-          st->ps = 0;
-          st->pe += st->W;
+    // Round-robin over the consumer rings, one chunk per ring per round,
+    // blocking (try_wait suspends in hardware) on the slot it needs next:
+    // consumers drain at similar rates, so each ring keeps S-1 chunks of slack.
+    for (;;) {
+      bool any = false;
+#pragma unroll
+      for (int w = 0; w < NCONS; ++w) {
+        const uint32_t c = issued[w];
+        if (c >= nchunks[w]) continue;
+        any = true;
+        const int slot = (int)(c % S);
+        if (c >= S)
+          while (!mbar_try_wait(&empty[w * S + slot], ((c / S) - 1) & 1u)) {
+          }
+        const Segment& sg = seg[ps[w]];
+        mbar_expect_tx(&full[w * S + slot], CH * 8u);
+        bulk_g2s(rings + (size_t)w * RING + slot * CH,
+                 sg.base + pe[w] * sg.stride + (int64_t)pq[w] * CH, CH * 8u,
+                 &full[w * S + slot], sg.keep ? pol_last : pol_first);
+        if (++pq[w] == sg.nch) {
+          pq[w] = 0;
+          do {
+            if (++ps[w] == nseg) {
+              ps[w] = 0;
+              pe[w] += W;
+            }
+          } while (seg[ps[w]].nch == 0);
         }
-      } while (st->seg[st->ps].nch == 0);
+        issued[w] = c + 1;
+      }
+      if (!any) break;
     }
   }
+};
 
-  // Slow path of the consumer's window check: release [.., a), refill,
-  // wait for [.., b).  Returns the new ready end (stream position up to
-  // which data has landed).
-  static __device__ __noinline__ uint32_t slow(RingState* st, uint32_t a, uint32_t b, int lane) {
-    uint32_t limit = a / CH + S;
-    const uint32_t nchunks = st->nchunks;
-    if (limit > nchunks) limit = nchunks;
-    const uint32_t issued = st->issued;
-    uint32_t waited = st->waited;
-    __syncwarp();  // every lane is done with the slots being refilled
-    if (lane == 0 && issued < limit) {
-      fence_proxy_async_smem();
-      for (uint32_t c = issued; c < limit; ++c) issue_next(st, c);
-      st->issued = limit;
+// Consumer side of one ring (all lanes, warp-uniform state in registers).
+template <int RING, int CH>
+struct Consumer {
+  static constexpr int S = RING / CH;
+  uint64_t* full;
+  uint64_t* empty;
+  uint32_t released = 0, waited = 0, ready_end = 0;
+
+  // make stream positions [.., b) readable, releasing every chunk before a
+  __device__ __forceinline__ void window(uint32_t a, uint32_t b, int lane) {
+    if (b <= ready_end) return;
+    const uint32_t rel = a / CH;
+    if (rel > released) {
+      __syncwarp();  // the whole warp is done with those slots
+      if (lane == 0)
+        for (uint32_t c = released; c < rel; ++c) mbar_arrive(&empty[c % S]);
+      released = rel;
     }
     while (waited * CH < b) {
-      const int slot = (int)(waited % S);
-      const uint32_t parity = (waited / S) & 1u;
-      while (!mbar_try_wait(&st->bar[slot], parity)) {
+      const uint32_t c = waited;
+      while (!mbar_try_wait(&full[c % S], (c / S) & 1u)) {
       }
       ++waited;
     }
-    __syncwarp();
-    if (lane == 0) st->waited = waited;
-    return waited * CH;
+    ready_end = waited * CH;
   }
 };
 
