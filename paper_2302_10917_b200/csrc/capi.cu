@@ -505,7 +505,15 @@ extern "C" int mh_get_element_schur(mh_system* s, int64_t first, int64_t count, 
     MH_CHECK_CUDA(cudaMemcpyAsync(out, s->S.p + first * blk, sizeof(double) * blk * count,
                                   cudaMemcpyDeviceToHost, s->stream));
   MH_CHECK_CUDA(cudaStreamSynchronize(s->stream));
-  // stored as +C A^-1 B; the reference's explicit block is its negative
-  for (size_t i = 0; i < blk * (size_t)count; ++i) out[i] = -out[i];
+  // stored transposed as +C A^-1 B; the reference's explicit block is
+  // -(C A^-1 B) in row-major order
+  const int nc = s->nc;
+  std::vector<double> tmp(blk);
+  for (int64_t b = 0; b < count; ++b) {
+    double* o = out + b * blk;
+    std::memcpy(tmp.data(), o, blk * sizeof(double));
+    for (int r = 0; r < nc; ++r)
+      for (int c = 0; c < nc; ++c) o[(size_t)r * nc + c] = -tmp[(size_t)c * nc + r];
+  }
   return MH_OK;
 }

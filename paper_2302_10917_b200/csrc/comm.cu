@@ -26,19 +26,6 @@ int halo_rhs_begin(mh_system* s) {
 
 void free_comm(mh_system* s) { (void)s; }
 
-int launch_element_schur(mh_system* s) {
-  (void)s;
-  set_error("mode mb: element Schur not implemented yet");
-  return MH_E_UNSUPPORTED;
-}
-
-int launch_element_mb(mh_system* s, const double* u) {
-  (void)s;
-  (void)u;
-  set_error("mode mb: element Schur not implemented yet");
-  return MH_E_UNSUPPORTED;
-}
-
 }  // namespace mh
 
 using namespace mh;

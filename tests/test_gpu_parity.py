@@ -276,3 +276,34 @@ def test_full_config_against_reference_samples(gpu, name):
     assert np.linalg.norm(r) <= 10 * cfg.tol * np.linalg.norm(P.apply_preconditioner(sys_, sys_.f_vec))
     # bitwise determinism at full size
     assert np.array_equal(w, P.apply_schur(sys_, prob["uhat"]))
+
+
+def test_mb_mode_solve_matches_mf(c1):
+    """Criterion 4 (test_acceptance.py:122-135): matrix-based and matrix-free
+    paths agree in iterations (+-1) and solution."""
+    prob, sys_, _ = c1
+    cfg_mf = P.SolverConfig(tol=1e-10, mode="mf")
+    cfg_mb = P.SolverConfig(tol=1e-10, mode="mb")
+    s_mf, _ = P.solve_condensed(sys_, cfg_mf)
+    s_mb, _ = P.solve_condensed(sys_, cfg_mb)
+    assert abs(s_mf.report.iterations - s_mb.report.iterations) <= 1
+    assert rel(s_mb.uhat, s_mf.uhat) <= SOLVE_TOL
+    rec = s_mb.report.to_record()
+    assert rec["mode"] == "mb" and rec["converged"] is True
+    assert rec["dof_global"] == sys_.zhat
+
+
+def test_element_schur_blocks_match_oracle(gpu):
+    """-S_e = -(C A^-1 B) per macro vs the oracle's explicit block (masked)."""
+    prob = S.make_problem(3, 2, 2, 3, seed=2)
+    sys_, _ = condense_problem(prob)
+    P.form_element_schur(sys_)
+    from paper_2302_10917_b200._lib import lib, ptr, check
+    nc = prob["nc"]
+    blocks = np.empty((prob["N"], nc, nc))
+    check(lib.mh_get_element_schur(sys_.handle, 0, prob["N"], ptr(blocks)))
+    o = SO.system_from_problem(prob).factorize()
+    import scipy.linalg as sla
+    for e in range(prob["N"]):
+        ref = -(o.C[e] @ sla.lu_solve(o.lu[e], o.B[e]))
+        assert np.abs(blocks[e] - ref).max() <= APPLY_TOL * np.abs(ref).max()
