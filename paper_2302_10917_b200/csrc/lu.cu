@@ -179,6 +179,197 @@ __global__ void __launch_bounds__(kLuThreads) lu_kernel(LuArgs g) {
   }
 }
 
+// opaque select: keeps "for a: if (a == x) r[a] = v" from being turned into
+// a dynamically indexed (local-memory) register array access
+__device__ __forceinline__ double osel(bool c, double x, double y) {
+  double r;
+  asm("{\n .reg .pred q;\n setp.ne.b32 q, %3, 0;\n selp.f64 %0, %1, %2, q;\n}"
+      : "=d"(r) : "d"(x), "d"(y), "r"((int)c));
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// Register-resident variant for Q <= 32 R <= NW NB: the whole block lives in
+// registers, lane l of warp w owning rows l + 32 a and columns w + NW b.
+// Column k is owned by warp k % NW, so the pivot search is a warp argmax and
+// the pivot row's values reach every warp with one shuffle per column; rows
+// are exchanged physically (LAPACK dgetf2 semantics) only when the pivot
+// actually moves.  One CTA barrier per column step publishes the pivot and
+// the multiplier column l (double-buffered in shared memory).
+template <int R, int NB, int NW>
+__global__ void __launch_bounds__(NW * 32, 512 / (NW * 32)) lu_reg_kernel(LuArgs g) {
+  __shared__ double lcol[2][32 * R];
+  __shared__ int s_p[2];
+  __shared__ int s_perm[32 * R];
+  __shared__ double red[NW];
+  static_assert(32 % NW == 0 || NW % 32 == 0, "NW must divide 32");
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t e = blockIdx.x;
+  const int Q = g.Q;
+  const double* __restrict__ Ae = g.A + e * (int64_t)Q * Q;
+
+  double A[R][NB];
+  double amax = 0.0;
+#pragma unroll
+  for (int a = 0; a < R; ++a)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int i = lane + 32 * a, j = w + NW * b;
+      const double v = (i < Q && j < Q) ? __ldg(Ae + (int64_t)i * Q + j) : 0.0;
+      A[a][b] = v;
+      amax = fmax(amax, fabs(v));
+    }
+  for (int o = 16; o; o >>= 1) amax = fmax(amax, __shfl_xor_sync(kFull, amax, o));
+  if (lane == 0) red[w] = amax;
+  for (int i = threadIdx.x; i < 32 * R; i += NW * 32) s_perm[i] = i;
+  __syncthreads();
+  amax = 0.0;
+#pragma unroll
+  for (int i = 0; i < NW; ++i) amax = fmax(amax, red[i]);
+  double dmin = DBL_MAX;  // min |U_kk| (owner lanes 0)
+
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+#pragma unroll 1
+    for (int kk = 0; kk < NW; ++kk) {
+      const int k = b * NW + kk;
+      if (k >= Q) break;
+      const int buf = k & 1;
+      // row k lives in register a = k / 32 = (NW b) / 32 (static: NW | 32 and
+      // kk < NW), lane k % 32
+      const int ak = (NW * b) >> 5, lk = k & 31;
+      if (w == kk) {
+        // ---- owner of column k: idamax over rows k..Q-1 (first index on ties)
+        double best = -1.0;
+        int bi = Q;
+#pragma unroll
+        for (int a = 0; a < R; ++a) {
+          const int i = lane + 32 * a;
+          const double v = fabs(A[a][b]);
+          if (i >= k && i < Q && v > best) { best = v; bi = i; }
+        }
+        for (int o = 16; o; o >>= 1) {
+          const double ov = __shfl_xor_sync(kFull, best, o);
+          const int oi = __shfl_xor_sync(kFull, bi, o);
+          if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+        }
+        const int p = bi;
+        // swap A[k][k] <-> A[p][k] inside this column
+        double colk_p = 0.0, colk_k = 0.0;
+#pragma unroll
+        for (int a = 0; a < R; ++a) {
+          const double vp = __shfl_sync(kFull, A[a][b], p & 31);
+          const double vk = __shfl_sync(kFull, A[a][b], lk);
+          colk_p = osel(a == (p >> 5), vp, colk_p);
+          if (a == ak) colk_k = vk;
+        }
+        const double pv = colk_p;
+        if (p != k && pv != 0.0) {
+#pragma unroll
+          for (int a = 0; a < R; ++a) {
+            if (a == ak) A[a][b] = osel(lane == lk, colk_p, A[a][b]);
+            A[a][b] = osel(a == (p >> 5) && lane == (p & 31), colk_k, A[a][b]);
+          }
+        }
+        // multipliers l_i = a_ik / pivot (reciprocal when |pivot| >= DBL_MIN)
+        const bool big = fabs(pv) >= DBL_MIN;
+        const double rcp = 1.0 / pv;
+#pragma unroll
+        for (int a = 0; a < R; ++a) {
+          const int i = lane + 32 * a;
+          double l = 0.0;
+          if (i > k && i < Q) {
+            if (pv != 0.0) A[a][b] = big ? A[a][b] * rcp : A[a][b] / pv;
+            l = A[a][b];
+          }
+          lcol[buf][i] = l;
+        }
+        if (lane == 0) {
+          s_p[buf] = (pv != 0.0) ? p : k;
+          g.piv[e * Q + k] = p;
+          if (p != k) {
+            const int tmp = s_perm[k];
+            s_perm[k] = s_perm[p];
+            s_perm[p] = tmp;
+          }
+          dmin = fmin(dmin, fabs(pv));
+        }
+      }
+      __syncthreads();
+      const int p = s_p[buf];
+      // ---- physical row exchange k <-> p in this warp's other columns
+      if (p != k) {
+#pragma unroll
+        for (int bb = 0; bb < NB; ++bb) {
+          if (w == kk && bb == b) continue;
+          double vk = 0.0, vp = 0.0;
+#pragma unroll
+          for (int a = 0; a < R; ++a) {
+            const double xp = __shfl_sync(kFull, A[a][bb], p & 31);
+            if (a == ak) vk = __shfl_sync(kFull, A[a][bb], lk);
+            vp = osel(a == (p >> 5), xp, vp);
+          }
+#pragma unroll
+          for (int a = 0; a < R; ++a) {
+            if (a == ak) A[a][bb] = osel(lane == lk, vp, A[a][bb]);
+            A[a][bb] = osel(a == (p >> 5) && lane == (p & 31), vk, A[a][bb]);
+          }
+        }
+      }
+      // ---- rank-1 update of the trailing columns j > k owned by this warp
+      double l[R];
+#pragma unroll
+      for (int a = 0; a < R; ++a) l[a] = lcol[buf][lane + 32 * a];
+#pragma unroll
+      for (int bb = b; bb < NB; ++bb) {
+        const int j = w + NW * bb;
+        if (j > k && j < Q) {  // warp-uniform
+          const double u = __shfl_sync(kFull, A[ak][bb], lk);
+#pragma unroll
+          for (int a = 0; a < R; ++a)
+            if (a >= ak) A[a][bb] = fma(-l[a], u, A[a][bb]);
+        }
+      }
+    }
+  }
+
+  // ---- outputs: packed L (columns ascending), packed U (columns
+  // descending), diag(U), 1/U_kk, permutation, singular flag
+  double* Lpe = g.Lp + e * g.ldL;
+  double* Upe = g.Up + e * g.ldL;
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const int j = w + NW * b;
+    if (j >= Q) continue;
+    const int64_t ol = off_lower(j, Q), ou = off_upper(j, Q);
+#pragma unroll
+    for (int a = 0; a < R; ++a) {
+      const int i = lane + 32 * a;
+      if (i >= Q) continue;
+      const double v = A[a][b];
+      if (i > j) Lpe[ol + (i - j - 1)] = v;
+      else if (i < j) Upe[ou + i] = v;
+      else {
+        g.udiag[e * Q + i] = v;
+        g.dinv[e * Q + i] = 1.0 / v;
+      }
+    }
+  }
+  for (int64_t i = (int64_t)Q * (Q - 1) / 2 + threadIdx.x; i < g.ldL; i += NW * 32) {
+    Lpe[i] = 0.0;
+    Upe[i] = 0.0;
+  }
+  __syncthreads();  // s_perm complete
+  for (int i = threadIdx.x; i < Q; i += NW * 32) g.perm[e * Q + i] = s_perm[i];
+  if (lane == 0) red[w] = dmin;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = DBL_MAX;
+    for (int i = 0; i < NW; ++i) m = fmin(m, red[i]);
+    g.stat[e] = (m <= 1e-13 * fmax(amax, 1e-300)) ? 1 : 0;
+  }
+}
+
 __global__ void unpack_lu_kernel(const double* __restrict__ Lp, const double* __restrict__ Up,
                                  const double* __restrict__ udiag, int64_t ldL, int Q,
                                  int64_t first, int64_t count, double* __restrict__ out) {
@@ -230,7 +421,6 @@ int launch_lu(mh_system* s, float* ms) {
     MH_CHECK_CUDA(cudaEventCreate(&e1));
     MH_CHECK_CUDA(cudaEventRecord(e0, s->stream));
   }
-  if (!use_smem) MH_CHECK(s->LU.alloc((size_t)s->N * s->Q * s->Q));
   LuArgs g;
   g.A = s->A.p;
   g.LU = s->LU.p;
@@ -244,7 +434,19 @@ int launch_lu(mh_system* s, float* ms) {
   g.ldL = s->ldL;
   g.Q = s->Q;
   g.use_smem = use_smem;
-  lu_kernel<<<(unsigned)s->N, kLuThreads, dyn, s->stream>>>(g);
+  const int Q = s->Q;
+  const unsigned grid = (unsigned)s->N;
+  if (Q <= 32) lu_reg_kernel<1, 4, 8><<<grid, 256, 0, s->stream>>>(g);
+  else if (Q <= 64) lu_reg_kernel<2, 8, 8><<<grid, 256, 0, s->stream>>>(g);
+  else if (Q <= 96) lu_reg_kernel<3, 12, 8><<<grid, 256, 0, s->stream>>>(g);
+  else if (Q <= 128) lu_reg_kernel<4, 8, 16><<<grid, 512, 0, s->stream>>>(g);
+  else {
+    if (!use_smem) {
+      MH_CHECK(s->LU.alloc((size_t)s->N * s->Q * s->Q));
+      g.LU = s->LU.p;
+    }
+    lu_kernel<<<grid, kLuThreads, dyn, s->stream>>>(g);
+  }
   MH_CHECK_CUDA(cudaGetLastError());
   if (ms) {
     MH_CHECK_CUDA(cudaEventRecord(e1, s->stream));
