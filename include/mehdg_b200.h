@@ -195,18 +195,36 @@ int mh_gmres_op(int device, void* stream, int64_t n, mh_op_fn apply, void* apply
 int mh_dot(void* stream, int64_t n, const double* x_dev, const double* y_dev, double* out_host);
 
 /* ---- multi-GPU (NCCL over NVLink) ------------------------------------- */
-/* Halo plan of one rank (from mh_slab_partition + the global tables):
- * the rank's trace vector is [owned faces | halo faces]; it sends owned
- * uhat segments and receives halo segments before the element kernel, then
- * returns halo v-slot contributions to their owners, which subtract them in
- * the reference's left-then-right order.  See DESIGN.md. */
-int mh_set_halo(mh_system* sys, int nranks, int rank,
-                const int32_t* send_face_host, const int32_t* send_count_host,
-                const int32_t* recv_count_host, const int32_t* vret_slot_host,
-                const int32_t* vret_count_host, const int32_t* vrecv_face_host,
+/* Slab decomposition: rank r owns macros
+ * [elem_begin[r], elem_begin[r+1]) and the unknown faces whose left
+ * (lower-id) macro it owns.  Its trace vector is [owned faces | halo faces];
+ * halo faces (right macro here, left macro on rank q) are grouped by owner q
+ * ascending, then by global face index.  Per apply:
+ *   1. uhat halo: rank q sends the owned segments listed in send_face (grouped
+ *      by destination, send_count[dest] each) and receives recv_count[src]
+ *      contiguous halo segments from each source;
+ *   2. element kernel on the local macros;
+ *   3. v return: the slot segments listed in vret_slot (grouped by owner,
+ *      vret_count[owner] each) go back to the face owners, which receive
+ *      vrecv_count[src] contiguous segments into extra v-slots and subtract
+ *      them second, i.e. in the reference's left-then-right order -- so the
+ *      multi-GPU apply is bitwise identical to the single-GPU one.
+ * Krylov dot products are all-gathered and summed in rank order.
+ * mh_set_halo must precede mh_upload_connectivity; face_elem entries >= the
+ * local macro count address received v-slot segments (N + j). */
+int mh_set_halo(mh_system* sys, int nranks, int rank, const int32_t* send_face_host,
+                const int32_t* send_count_host, const int32_t* recv_count_host,
+                const int32_t* vret_slot_host, const int32_t* vret_count_host,
                 const int32_t* vrecv_count_host);
-/* ncclUniqueId bytes (128) shared by all ranks; rank 0 creates it. */
+/* Apply the operator of a slab-partitioned problem held by n systems in ONE
+ * process (system r = rank r, halo plans set, no communicator): the same
+ * pack / exchange / element / v-return / face phases as the NCCL path, with
+ * the exchanges done by device-to-device copies.  Used to verify the halo
+ * plans and kernels on a single GPU; u_dev[r] / w_dev[r] are rank-local. */
+int mh_group_apply(mh_system** systems, int n, const double** u_dev, double** w_dev);
+/* ncclUniqueId bytes (128); rank 0 creates it and the caller broadcasts it. */
 int mh_comm_unique_id(void* id_out_128);
+/* NCCL communicator over all ranks (libnccl.so.2 is loaded at run time). */
 int mh_comm_init(mh_system* sys, const void* id_128, int nranks, int rank);
 
 #ifdef __cplusplus

@@ -82,7 +82,8 @@ SIGNATURES = {
     "mh_gmres_op": [C.c_int, _p, C.c_int64, OP_FN, _p, OP_FN, _p, C.c_double, C.c_int, C.c_int,
                     _dp, _dp, _ip, _ip, _dp, C.c_int, _ip],
     "mh_dot": [_p, C.c_int64, _dp, _dp, C.POINTER(C.c_double)],
-    "mh_set_halo": [_p, C.c_int, C.c_int, _p, _p, _p, _p, _p, _p, _p],
+    "mh_set_halo": [_p, C.c_int, C.c_int, _p, _p, _p, _p, _p, _p],
+    "mh_group_apply": [C.POINTER(_p), C.c_int, C.POINTER(_p), C.POINTER(_p)],
     "mh_comm_unique_id": [_p],
     "mh_comm_init": [_p, _p, C.c_int, C.c_int],
 }

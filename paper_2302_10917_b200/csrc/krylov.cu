@@ -70,7 +70,8 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 __global__ void __launch_bounds__(kDotThreads)
 dot_kernel(int64_t n, double* __restrict__ w, const double* __restrict__ Vp,
            const double* __restrict__ coef, const double* __restrict__ Vi, int mode,
-           double* __restrict__ part, unsigned* __restrict__ ticket, double* __restrict__ out) {
+           bool take_sqrt, double* __restrict__ part, unsigned* __restrict__ ticket,
+           double* __restrict__ out) {
   __shared__ double red[kDotThreads / 32];
   __shared__ bool last;
   const int64_t b = blockIdx.x;
@@ -101,7 +102,7 @@ dot_kernel(int64_t n, double* __restrict__ w, const double* __restrict__ Vp,
   for (int i = threadIdx.x; i < kDotBlocks; i += kDotThreads) v += ((volatile double*)part)[i];
   const double tot = block_sum(v, red);
   if (threadIdx.x == 0) {
-    *out = (mode == 2) ? sqrt(tot) : tot;
+    *out = (mode == 2 && take_sqrt) ? sqrt(tot) : tot;
     *ticket = 0u;
   }
 }
@@ -158,11 +159,17 @@ struct OpFn {
   }
 };
 
+// Dot product (and fused MGS update).  With a multi-GPU system the local
+// sum is all-gathered and added in rank order, identically on every rank.
+thread_local mh_system* g_comm_sys = nullptr;  // bound for the duration of one solve
+
 int dot_dev(cudaStream_t st, Krylov* K, int64_t n, double* w, const double* Vp,
             const double* coef, const double* Vi, int mode, double* out) {
-  dot_kernel<<<kDotBlocks, kDotThreads, 0, st>>>(n, w, Vp, coef, Vi, mode, K->part.p,
-                                                  K->ticket.p, out);
+  const bool multi = g_comm_sys && g_comm_sys->nranks > 1;
+  dot_kernel<<<kDotBlocks, kDotThreads, 0, st>>>(n, w, Vp, coef, Vi, mode, !multi, K->part.p,
+                                                  K->ticket.p, multi ? K->scal.p + 3 : out);
   MH_CHECK_CUDA(cudaGetLastError());
+  if (multi) MH_CHECK(allreduce_scalar(g_comm_sys, K->scal.p + 3, out, mode == 2));
   return MH_OK;
 }
 
@@ -180,6 +187,16 @@ int apply_MA(const OpFn& A, const OpFn& M, const OpFn& MA, const double* v, doub
   MH_CHECK(A(v, scratch));
   return M(scratch, z);
 }
+
+int gmres_core(cudaStream_t st, Krylov* K, int64_t n, const OpFn& A, const OpFn& M,
+               const OpFn& MA, double tol, int restart, int maxiter, const double* rhs,
+               double* x, int* iterations, int* converged, double* hist_host, int hist_cap,
+               int* hist_len);
+
+struct CommScope {  // binds the communicator of a system to the dot products
+  explicit CommScope(mh_system* s) { g_comm_sys = s; }
+  ~CommScope() { g_comm_sys = nullptr; }
+};
 
 int gmres_core(cudaStream_t st, Krylov* K, int64_t n, const OpFn& A, const OpFn& M,
                const OpFn& MA, double tol, int restart, int maxiter, const double* rhs,
@@ -349,7 +366,7 @@ extern "C" int mh_dot(void* stream, int64_t n, const double* x, const double* y,
   MH_CHECK(K.scal.alloc(1));
   MH_CHECK_CUDA(cudaMemsetAsync(K.ticket.p, 0, sizeof(unsigned), st));
   dot_kernel<<<kDotBlocks, kDotThreads, 0, st>>>(n, const_cast<double*>(x), nullptr, nullptr, y, 0,
-                                                  K.part.p, K.ticket.p, K.scal.p);
+                                                  true, K.part.p, K.ticket.p, K.scal.p);
   MH_CHECK_CUDA(cudaGetLastError());
   MH_CHECK_CUDA(cudaMemcpyAsync(out, K.scal.p, sizeof(double), cudaMemcpyDeviceToHost, st));
   MH_CHECK_CUDA(cudaStreamSynchronize(st));
@@ -399,6 +416,7 @@ extern "C" int mh_gmres(mh_system* s, double tol, int restart, int maxiter, int 
       MA.ctx = s;
     }
   }
+  CommScope scope(s);
   return gmres_core(s->stream, s->kry, n, A, M, MA, tol, restart, maxiter, rhs, x, iterations,
                     converged, hist_host, hist_cap, hist_len);
 }

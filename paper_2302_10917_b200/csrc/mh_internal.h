@@ -127,9 +127,14 @@ struct mh_system {
   std::vector<cudaEvent_t> ev_pool;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_elem, ev_face;
 
-  // multi-GPU
+  // multi-GPU (comm.cu)
   int nranks = 1, rank = 0;
   void* nccl = nullptr;  // ncclComm_t
+  bool have_halo = false;
+  std::vector<int32_t> send_count, recv_count, vret_count, vrecv_count;  // per peer
+  mh::DBuf<int32_t> send_face, vret_slot;
+  mh::DBuf<double> sendbuf, vsendbuf;
+  mh::DBuf<double> dot_local, dot_all;  // Krylov all-gather scratch
 };
 
 namespace mh {
@@ -157,4 +162,6 @@ int halo_u_exchange(mh_system* s, const double* u, const double** u_halo);
 int halo_v_exchange(mh_system* s);
 int halo_rhs_begin(mh_system* s);
 void free_comm(mh_system* s);
+// sum a device scalar over ranks (rank order) into out; sqrt if requested
+int allreduce_scalar(mh_system* s, const double* local, double* out, bool take_sqrt);
 }  // namespace mh
