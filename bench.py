@@ -202,7 +202,7 @@ def config_block(name, prob, world):
             "F_unknown": prob["F"], "zhat": prob["zhat"],
             "operator": "matrix-free D - C A^-1 B (C = B^T synthetic, B_e streamed once)",
             "l2_flush": "none needed: 3.2 GB of blocks per apply >> 126 MB L2",
-            "parallelism": f"replicas{world}" if world > 1 else "single"}
+            "parallelism": f"slabs{world} (NCCL halo)" if world > 1 else "single"}
 
 
 def run_reference(args, world, rank):
@@ -247,44 +247,75 @@ def run_reference(args, world, rank):
     return 0
 
 
+def build_local(args, world, rank, dev):
+    """This rank's system: the whole problem at N=1, its slab at N>1."""
+    import numpy as np
+
+    import paper_2302_10917_b200 as P
+    from paper_2302_10917_b200 import synthetic as S
+
+    d, n, m, p = S.CONFIGS[args.config]
+    t0 = time.perf_counter()
+    if world == 1:
+        prob = S.make_problem(d, n, m, p, seed=args.seed)
+        t_gen = time.perf_counter() - t0
+        tables = {"nfe": d + 1, "elem_ufac": prob["elem_face"], "face_elem": prob["face_elem"],
+                  "face_slot": prob["face_slot"], "uidx": prob["uidx"], "F": prob["F"]}
+        cfg = P.SolverConfig(tol=1e-10, device=dev)
+        t0 = time.perf_counter()
+        sys_ = P.condense_arrays(prob["mesh"], prob["A"], None, prob["Be"], prob["R_u"],
+                                 prob["D"], prob["R_hat"], cfg, tables=tables, device=dev)
+        return prob, sys_, None, t_gen, time.perf_counter() - t0
+    from paper_2302_10917_b200.distributed import RankSystem, broadcast_unique_id, local_trace
+    from paper_2302_10917_b200.partition import partition, rank_plan
+
+    prob = S.make_problem(d, n, m, p, seed=args.seed, with_blocks=False)
+    eb = partition(d, n, prob["N"], world)
+    plan = rank_plan(prob["elem_face"], prob["face_elem"], prob["face_slot"], eb, rank)
+    A, Be, Ru = S.gen_macros(prob["N"], prob["Q"], prob["nc"], args.seed, plan.e0, plan.n_local)
+    D = S.gen_faces(prob["F"], prob["t"], args.seed)[plan.owned]
+    uh = S.gen_uhat(prob["zhat"], args.seed)
+    prob["uhat_local"] = local_trace(uh, plan, prob["t"])
+    t_gen = time.perf_counter() - t0
+    cid = broadcast_unique_id(rank, dev)
+    t0 = time.perf_counter()
+    rs = RankSystem(prob, plan, device=dev, comm_id=cid,
+                    blocks=dict(A=A, Be=Be, R_u=Ru, D=D, R_hat=np.zeros((plan.F_own, prob["t"]))))
+    return prob, rs, plan, t_gen, time.perf_counter() - t0
+
+
 def run_ours(args, world, rank, local):
     import ctypes as C
 
     import torch
 
     import paper_2302_10917_b200 as P
-    from paper_2302_10917_b200 import _lib, synthetic as S
+    from paper_2302_10917_b200 import synthetic as S
     from paper_2302_10917_b200._lib import check, lib, ptr
 
     dev = local
     torch.cuda.set_device(dev)
-    d, n, m, p = S.CONFIGS[args.config]
-    t0 = time.perf_counter()
-    prob = S.make_problem(d, n, m, p, seed=args.seed)
-    t_gen = time.perf_counter() - t0
-    tables = {"nfe": d + 1, "elem_ufac": prob["elem_face"], "face_elem": prob["face_elem"],
-              "face_slot": prob["face_slot"], "uidx": prob["uidx"], "F": prob["F"]}
-    cfg = P.SolverConfig(tol=1e-10, device=dev)
-    t0 = time.perf_counter()
-    sys_ = P.condense_arrays(prob["mesh"], prob["A"], None, prob["Be"], prob["R_u"], prob["D"],
-                             prob["R_hat"], cfg, tables=tables, device=dev)
-    t_condense = time.perf_counter() - t0
+    prob, sys_, plan, t_gen, t_condense = build_local(args, world, rank, dev)
     h = sys_.handle
     stream = torch.cuda.current_stream(dev)
+    d = prob["d"]
     N, Q, nc, t, F = prob["N"], prob["Q"], prob["nc"], prob["t"], prob["F"]
+    N_loc = N if plan is None else plan.n_local
+    F_loc = F if plan is None else plan.F_own
 
-    # ---- batched LU ----------------------------------------------------------
+    # ---- batched LU (this rank's blocks) ------------------------------------
     lu_ms = []
     for i in range(4):
         ms = C.c_float()
         check(lib.mh_refactorize_local(h, C.byref(ms)), "lu")
         if i:
             lu_ms.append(ms.value)
-    lu_ms = float(np.mean(lu_ms))
+    lu_ms = max_over_ranks(float(sum(lu_ms) / len(lu_ms)), world)
     lu_flops = S.lu_flops(N, Q)
 
     # ---- device-resident applies --------------------------------------------
-    u = torch.as_tensor(prob["uhat"], device=f"cuda:{dev}")
+    u_host = prob["uhat"] if plan is None else prob["uhat_local"]
+    u = torch.as_tensor(u_host, device=f"cuda:{dev}")
     w = torch.empty_like(u)
     for _ in range(args.warmup):
         check(lib.mh_apply(h, ptr(u), ptr(w)), "apply")
@@ -313,10 +344,10 @@ def run_ours(args, world, rank, local):
     sampler.stop()
     elapsed_ms = max_over_ranks(elapsed_ms, world)
     ms_per_step = elapsed_ms / args.steps
-    value = world * 1e3 / ms_per_step
+    value = 1e3 / ms_per_step  # applies/s of the whole (global) operator
 
     bytes_apply = S.algorithmic_bytes_per_apply(N, Q, nc, d, F, t)
-    elem_bytes = N * (8 * Q * Q + 4 * Q + 8 * nc * Q + 16 * nc + 4 * (d + 1))
+    elem_bytes = N_loc * (8 * Q * Q + 4 * Q + 8 * nc * Q + 16 * nc + 4 * (d + 1))
     elem_avg_ms = el_ms.value / max(el_n.value, 1)
     face_avg_ms = fa_ms.value / max(fa_n.value, 1)
     peaks = measured_peaks()
@@ -330,39 +361,55 @@ def run_ours(args, world, rank, local):
             traffic = None
 
     # ---- end-to-end through the public API (pinned host buffers) -------------
-    u_pin = torch.empty(prob["zhat"], dtype=torch.float64, pin_memory=True)
-    u_pin.copy_(torch.from_numpy(prob["uhat"]))
-    u_host = u_pin.numpy()
+    u_pin = torch.empty(u.numel(), dtype=torch.float64, pin_memory=True)
+    u_pin.copy_(torch.from_numpy(u_host))
+    w_pin = torch.empty_like(u_pin)
     e2e_steps = max(3, min(args.steps, 200))
+
+    def e2e_step():
+        if plan is None:
+            return P.apply_schur(sys_, u_pin.numpy())  # numpy in -> numpy out (H2D + D2H inside)
+        ud = u_pin.to(f"cuda:{dev}", non_blocking=True)
+        wd = sys_.apply(ud)
+        w_pin.copy_(wd, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+        return w_pin
+
     for _ in range(2):
-        P.apply_schur(sys_, u_host)
+        e2e_step()
     barrier(world)
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
     e0.record(stream)
     for _ in range(e2e_steps):
-        w_host = P.apply_schur(sys_, u_host)
+        e2e_step()
     e1.record(stream)
     torch.cuda.synchronize(dev)
     e2e_wall = time.perf_counter() - t0
     e2e_ms = max_over_ranks(max(e0.elapsed_time(e1), e2e_wall * 1e3) / e2e_steps, world)
-    assert w_host.shape == (prob["zhat"],)
 
     # ---- full solve (GMRES + D^-1 to 1e-10) ----------------------------------
     torch.cuda.synchronize(dev)
+    barrier(world)
     t0 = time.perf_counter()
-    x, info = P.gmres(P.SchurOperator(sys_), sys_.f_device, cfg, precond=P.Preconditioner(sys_))
+    if plan is None:
+        cfg = P.SolverConfig(tol=1e-10, device=dev)
+        x, info = P.gmres(P.SchurOperator(sys_), sys_.f_device, cfg,
+                          precond=P.Preconditioner(sys_))
+    else:
+        x, info = sys_.gmres(tol=1e-10)
     torch.cuda.synchronize(dev)
-    t_solve = time.perf_counter() - t0
+    t_solve = max_over_ranks(time.perf_counter() - t0, world)
 
     line = {
         "metric": BASELINE_METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded BASELINE generator, numpy PCG64; blocks resident in HBM)",
         "config": config_block(args.config, prob, world),
         "hbm_gbs": bytes_apply / (ms_per_step * 1e-3) / 1e9,
-        "hbm_frac": bytes_apply / (ms_per_step * 1e-3) / 1e9 / peaks["hbm_gbs"],
+        "hbm_frac": bytes_apply / (ms_per_step * 1e-3) / 1e9 / (peaks["hbm_gbs"] * world),
         "bytes_per_apply": bytes_apply,
         "roofline": {"bound": "hbm", "kernel": "element_kernel (gather+B^T+LU solve+C, per macro)",
                      "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
@@ -371,7 +418,8 @@ def run_ours(args, world, rank, local):
                      "face_kernel_avg_ms": face_avg_ms, "peak_source": peaks["source"]},
         "e2e": {"value": 1e3 / e2e_ms, "unit": UNIT, "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": prob["zhat"] * 8, "d2h_bytes_per_step": prob["zhat"] * 8,
-                "api": "paper_2302_10917_b200.apply_schur(sys, numpy pinned uhat)"},
+                "api": "paper_2302_10917_b200.apply_schur(sys, numpy pinned uhat)"
+                if plan is None else "RankSystem.apply with pinned host copies per rank"},
         "gpu_launches": int(el_n.value + fa_n.value),
         "lu": {"gflops": lu_flops / (lu_ms * 1e-3) / 1e9, "ms": lu_ms, "flops": lu_flops,
                "bytes": 16 * N * Q * Q, "gbs": 16 * N * Q * Q / (lu_ms * 1e-3) / 1e9},
@@ -380,7 +428,7 @@ def run_ours(args, world, rank, local):
         "setup_s": {"generate": t_gen, "condense": t_condense},
         "clocks": sampler.summary(),
     }
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = time_oracle(prob, args.cpu_sample, reps=args.cpu_reps, threads=1)
         line["cpu_baseline"] = {
             "value": cb["applies_per_s"], "unit": UNIT, "cores": 1, "kind": "port",
