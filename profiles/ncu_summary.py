@@ -31,20 +31,26 @@ def main(rep, top=25):
         for k in KEYS:
             if k in d:
                 print(f"  {k} = {d[k][0]} {d[k][1]}")
-        st = [(h, float(v[0])) for h, v in d.items()
-              if h.startswith("smsp__average_warps_issue_stalled") and
-              h.endswith("per_issue_active.ratio") and v[0] not in ("", "n/a")]
+        st = []
+        for h, v in d.items():
+            if h.startswith("smsp__average_warps_issue_stalled") and \
+                    h.endswith("per_issue_active.ratio"):
+                try:
+                    st.append((h, float(v[0])))
+                except ValueError:
+                    pass
         for h, v in sorted(st, key=lambda x: -x[1])[:8]:
             print(f"  stall {h.split('stalled_')[1].split('_per')[0]} = {v:.2f}")
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=sass"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    if len(rows) > 2:
+    if top and len(rows) > 2:
         hdr = rows[1]
         data = rows[2:]
         i_src = hdr.index("Source")
         i_s = hdr.index("Warp Stall Sampling (All Samples)")
-        tot = sum(float(r[i_s] or 0) for r in data if len(r) > i_s)
+        data = [r for r in data if len(r) > i_s and r[i_s].replace(".", "").isdigit()]
+        tot = sum(float(r[i_s] or 0) for r in data)
         print(f"  sampled stalls: {tot:.0f}")
         for r in sorted(data, key=lambda r: -float(r[i_s] or 0))[:top]:
             print(f"   {float(r[i_s]) / tot * 100:5.1f}%  {r[i_src].strip()[:90]}")
