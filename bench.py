@@ -388,16 +388,23 @@ def run_ours(args, world, rank, local):
     e2e_wall = time.perf_counter() - t0
     e2e_ms = max_over_ranks(max(e0.elapsed_time(e1), e2e_wall * 1e3) / e2e_steps, world)
 
-    # ---- full solve (GMRES + D^-1 to 1e-10) ----------------------------------
+    # ---- full solve (GMRES + D^-1 to 1e-10); the first call allocates the
+    # Krylov basis, the second is timed ----------------------------------------
+    def run_solve():
+        if plan is None:
+            cfg = P.SolverConfig(tol=1e-10, device=dev)
+            return P.gmres(P.SchurOperator(sys_), sys_.f_device, cfg,
+                           precond=P.Preconditioner(sys_))
+        return sys_.gmres(tol=1e-10)
+
     torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    run_solve()
+    torch.cuda.synchronize(dev)
+    t_solve_first = time.perf_counter() - t0
     barrier(world)
     t0 = time.perf_counter()
-    if plan is None:
-        cfg = P.SolverConfig(tol=1e-10, device=dev)
-        x, info = P.gmres(P.SchurOperator(sys_), sys_.f_device, cfg,
-                          precond=P.Preconditioner(sys_))
-    else:
-        x, info = sys_.gmres(tol=1e-10)
+    x, info = run_solve()
     torch.cuda.synchronize(dev)
     t_solve = max_over_ranks(time.perf_counter() - t0, world)
 
@@ -424,7 +431,8 @@ def run_ours(args, world, rank, local):
         "lu": {"gflops": lu_flops / (lu_ms * 1e-3) / 1e9, "ms": lu_ms, "flops": lu_flops,
                "bytes": 16 * N * Q * Q, "gbs": 16 * N * Q * Q / (lu_ms * 1e-3) / 1e9},
         "solve": {"iterations": info["iterations"], "converged": info["converged"],
-                  "seconds": t_solve, "tol": 1e-10},
+                  "seconds": t_solve, "ms_per_iteration": t_solve * 1e3 / max(info["iterations"], 1),
+                  "first_call_seconds": t_solve_first, "tol": 1e-10},
         "setup_s": {"generate": t_gen, "condense": t_condense},
         "clocks": sampler.summary(),
     }

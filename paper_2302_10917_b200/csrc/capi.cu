@@ -142,8 +142,7 @@ extern "C" int mh_destroy(mh_system* s) {
   s->A.release(); s->LU.release(); s->Lp.release(); s->Up.release(); s->udiag.release();
   s->dinv.release(); s->piv.release(); s->perm.release();
   s->lstat.release(); s->Bt.release(); s->Cm.release(); s->Ru.release(); s->D.release();
-  s->Draw.release(); s->Rhat.release(); s->FL.release(); s->FU.release(); s->FrL.release();
-  s->FrU.release(); s->Fperm.release(); s->Fsign.release(); s->Fkind.release(); s->V.release();
+  s->Draw.release(); s->Rhat.release(); s->Dinv.release(); s->Fkind.release(); s->V.release();
   s->tmp.release(); s->S.release(); s->halo_u.release(); s->hin.release(); s->hout.release();
   if (s->kry) free_krylov(s->kry);
   free_comm(s);
@@ -229,12 +228,7 @@ static int alloc_blocks(mh_system* s) {
   MH_CHECK(s->D.alloc(F * t * t));
   MH_CHECK(s->Draw.alloc(F * t * t));
   MH_CHECK(s->Rhat.alloc(F * t));
-  MH_CHECK(s->FL.alloc(F * t * t));
-  MH_CHECK(s->FU.alloc(F * t * t));
-  MH_CHECK(s->FrL.alloc(F * t));
-  MH_CHECK(s->FrU.alloc(F * t));
-  MH_CHECK(s->Fperm.alloc(F * t));
-  MH_CHECK(s->Fsign.alloc(F));
+  MH_CHECK(s->Dinv.alloc(F * t * t));
   MH_CHECK(s->Fkind.alloc(F));
   MH_CHECK(s->V.alloc((N * s->nfe + (size_t)s->n_vslot_extra) * t));
   MH_CHECK(s->tmp.alloc((F + (size_t)s->F_halo) * t + 1));

@@ -10,11 +10,13 @@
 //                       (schur_solver.py:247-253); optionally fused with
 //                       the D^-1 preconditioner (the GMRES M(A v) step).
 //   precond_kernel      apply_preconditioner (schur_solver.py:296-305):
-//                       z_f = sign * U^-1 L^-1 P w_f.
+//                       z_f = D_f^-1 w_f.
 //
-// Face data layout: D column-major (t x t), factors FL (lower, diag = L_jj
-// for Cholesky, unit for LU) and FU (upper) column-major, reciprocal
-// diagonals, permutation, sign.
+// The factor kernel turns the accepted factorisation (sign * L L^T, or
+// P D = L U) into the explicit inverse D_f^-1 (t right-hand sides solved by
+// the lanes of the warp), so the preconditioner is a GEMV with independent,
+// coalesced loads instead of a chain of 2t dependent substitution steps.
+// Face data layout: D and D^-1 column-major (t x t).
 
 #include <cfloat>
 
@@ -32,68 +34,32 @@ struct FaceArgs {
   const double* V;
   const double* uhat;
   double* out;
-  const double* FL;
-  const double* FU;
-  const double* FrL;
-  const double* FrU;
-  const int32_t* Fperm;
-  const double* Fsign;
+  const double* Dinv;
   int64_t F;
   int t;
 };
 
-// In-warp solve z <- sign * U^-1 L^-1 P z for face f (rows lane + 32 r).
+// z <- M z for the column-major t x t matrix M (rows lane + 32 r); the input
+// vector is staged in the warp's shared buffer sw
 template <int RT>
-__device__ __forceinline__ void face_solve(double (&z)[RT], const FaceArgs& a, int64_t f,
-                                           double* sw, int lane) {
-  const int t = a.t;
-  const size_t TT = (size_t)t * t;
+__device__ __forceinline__ void warp_gemv(double (&z)[RT], const double* __restrict__ M, int t,
+                                          double* sw, int lane) {
 #pragma unroll
   for (int r = 0; r < RT; ++r)
     if (lane + 32 * r < t) sw[lane + 32 * r] = z[r];
   __syncwarp();
-  double rl[RT], ru[RT];
 #pragma unroll
-  for (int r = 0; r < RT; ++r) {
-    const int i = lane + 32 * r;
-    z[r] = i < t ? sw[__ldg(a.Fperm + f * t + i)] : 0.0;
-    rl[r] = i < t ? __ldg(a.FrL + f * t + i) : 0.0;
-    ru[r] = i < t ? __ldg(a.FrU + f * t + i) : 0.0;
+  for (int r = 0; r < RT; ++r) z[r] = 0.0;
+#pragma unroll 8
+  for (int s = 0; s < t; ++s) {  // sum over s ascending
+    const double ws = sw[s];
+#pragma unroll
+    for (int r = 0; r < RT; ++r) {
+      const int i = lane + 32 * r;
+      if (i < t) z[r] = fma(__ldg(M + (size_t)s * t + i), ws, z[r]);
+    }
   }
   __syncwarp();
-  const double* L = a.FL + f * TT;
-  const double* U = a.FU + f * TT;
-#pragma unroll
-  for (int jb = 0; jb < RT; ++jb)
-    for (int jj = 0; jj < 32; ++jj) {
-      const int j = jb * 32 + jj;
-      if (j < t) {
-        if (lane == jj) z[jb] *= rl[jb];
-        const double zj = __shfl_sync(kFull, z[jb], jj);
-#pragma unroll
-        for (int r = jb; r < RT; ++r) {
-          const int i = lane + 32 * r;
-          if (i > j && i < t) z[r] = fma(-__ldg(L + (size_t)j * t + i), zj, z[r]);
-        }
-      }
-    }
-#pragma unroll
-  for (int jb = RT - 1; jb >= 0; --jb)
-    for (int jj = 31; jj >= 0; --jj) {
-      const int j = jb * 32 + jj;
-      if (j < t) {
-        if (lane == jj) z[jb] *= ru[jb];
-        const double zj = __shfl_sync(kFull, z[jb], jj);
-#pragma unroll
-        for (int r = 0; r <= jb; ++r) {
-          const int i = lane + 32 * r;
-          if (i < j) z[r] = fma(-__ldg(U + (size_t)j * t + i), zj, z[r]);
-        }
-      }
-    }
-  const double sg = __ldg(a.Fsign + f);
-#pragma unroll
-  for (int r = 0; r < RT; ++r) z[r] *= sg;
 }
 
 template <int RT, bool RHS, bool PRE>
@@ -103,30 +69,15 @@ __global__ void __launch_bounds__(kFaceWarps * 32) face_reduce_kernel(FaceArgs a
   const int64_t f = (int64_t)blockIdx.x * kFaceWarps + w;
   if (f >= a.F) return;
   const int t = a.t;
+  const size_t TT = (size_t)t * t;
   double* sw = s_buf + w * t;
   double z[RT];
-  if (RHS) {
 #pragma unroll
-    for (int r = 0; r < RT; ++r) {
-      const int i = lane + 32 * r;
-      z[r] = i < t ? __ldg(a.Rhat + f * t + i) : 0.0;
-    }
-  } else {
-    for (int s = lane; s < t; s += 32) sw[s] = __ldg(a.uhat + f * t + s);
-    __syncwarp();
-#pragma unroll
-    for (int r = 0; r < RT; ++r) z[r] = 0.0;
-    const double* Df = a.D + f * (size_t)t * t;
-    for (int s = 0; s < t; ++s) {  // (D uhat)_i, summed over s ascending
-      const double us = sw[s];
-#pragma unroll
-      for (int r = 0; r < RT; ++r) {
-        const int i = lane + 32 * r;
-        if (i < t) z[r] = fma(__ldg(Df + (size_t)s * t + i), us, z[r]);
-      }
-    }
-    __syncwarp();
+  for (int r = 0; r < RT; ++r) {
+    const int i = lane + 32 * r;
+    z[r] = i < t ? __ldg((RHS ? a.Rhat : a.uhat) + f * t + i) : 0.0;
   }
+  if (!RHS) warp_gemv<RT>(z, a.D + f * TT, t, sw, lane);  // D_f uhat_f
   const int sl = __ldg(a.vslot + 2 * f), sr = __ldg(a.vslot + 2 * f + 1);
 #pragma unroll
   for (int r = 0; r < RT; ++r) {
@@ -136,7 +87,7 @@ __global__ void __launch_bounds__(kFaceWarps * 32) face_reduce_kernel(FaceArgs a
       if (sr >= 0) z[r] -= __ldg(a.V + (int64_t)sr * t + i);  // then right
     }
   }
-  if (PRE) face_solve<RT>(z, a, f, sw, lane);
+  if (PRE) warp_gemv<RT>(z, a.Dinv + f * TT, t, sw, lane);
 #pragma unroll
   for (int r = 0; r < RT; ++r) {
     const int i = lane + 32 * r;
@@ -157,7 +108,7 @@ __global__ void __launch_bounds__(kFaceWarps * 32) precond_kernel(FaceArgs a) {
     const int i = lane + 32 * r;
     z[r] = i < t ? __ldg(a.uhat + f * t + i) : 0.0;
   }
-  face_solve<RT>(z, a, f, s_buf + w * t, lane);
+  warp_gemv<RT>(z, a.Dinv + f * (size_t)t * t, t, s_buf + w * t, lane);
 #pragma unroll
   for (int r = 0; r < RT; ++r) {
     const int i = lane + 32 * r;
@@ -241,18 +192,51 @@ __device__ void warp_lu(double* S, int t, int lane, int* perm) {
   }
 }
 
+// Column j of D^-1 for each lane j (< t, in chunks of 32): solve with the
+// factor in S.  chol: sign * (L L^T)^-1 e_j;  lu: U^-1 L^-1 P e_j.
+__device__ void warp_inverse(const double* S, const int* pm, int t, bool chol, double sign,
+                             double* scratch, double* out, int lane) {
+  for (int j0 = 0; j0 < t; j0 += 32) {
+    const int j = j0 + lane;
+    const bool act = j < t;
+    double* x = scratch + lane;  // x[i * 32]: this lane's column
+    if (act) {
+      for (int i = 0; i < t; ++i) x[i * 32] = chol ? (i == j ? 1.0 : 0.0) : (pm[i] == j ? 1.0 : 0.0);
+      // forward: L y = b (L lower; unit diagonal for LU)
+      for (int k = 0; k < t; ++k) {
+        double yk = x[k * 32];
+        if (chol) {
+          yk /= S[(size_t)k * t + k];
+          x[k * 32] = yk;
+        }
+        for (int i = k + 1; i < t; ++i) x[i * 32] = fma(-S[(size_t)k * t + i], yk, x[i * 32]);
+      }
+      // backward: L^T x = y (chol) or U x = y (lu), column-oriented
+      for (int k = t - 1; k >= 0; --k) {
+        const double xk = x[k * 32] / S[(size_t)k * t + k];
+        x[k * 32] = xk;
+        for (int i = 0; i < k; ++i) {
+          const double uik = chol ? S[(size_t)i * t + k] : S[(size_t)k * t + i];
+          x[i * 32] = fma(-uik, xk, x[i * 32]);
+        }
+      }
+      for (int i = 0; i < t; ++i) out[(size_t)j * t + i] = sign * x[i * 32];
+    }
+    __syncwarp();
+  }
+}
+
 __global__ void face_factor_kernel(const double* __restrict__ Drm, double* __restrict__ Dcm,
-                                   double* __restrict__ FL, double* __restrict__ FU,
-                                   double* __restrict__ FrL, double* __restrict__ FrU,
-                                   int32_t* __restrict__ Fperm, double* __restrict__ Fsign,
-                                   int8_t* __restrict__ Fkind, int64_t F, int t, int wpb) {
+                                   double* __restrict__ Dinv, int8_t* __restrict__ Fkind,
+                                   int64_t F, int t, int wpb) {
   extern __shared__ double s_fac[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t f = (int64_t)blockIdx.x * wpb + w;
   if (f >= F) return;
   const size_t TT = (size_t)t * t;
-  double* S = s_fac + (size_t)w * (TT + 64);
+  double* S = s_fac + (size_t)w * (TT + 64 + 32 * (size_t)t);
   int* pm = reinterpret_cast<int*>(S + TT);
+  double* scratch = S + TT + 64;
   const double* Df = Drm + f * TT;
   double dmax = 0.0;
   for (size_t idx = lane; idx < TT; idx += 32) {  // row-major in -> column-major copy
@@ -275,23 +259,7 @@ __global__ void face_factor_kernel(const double* __restrict__ Drm, double* __res
     if (warp_cholesky(S, t, lane)) kind = attempt == 0 ? MH_FACE_CHOL_NEG : MH_FACE_CHOL_POS;
     __syncwarp();
   }
-  double* FLf = FL + f * TT;
-  double* FUf = FU + f * TT;
-  if (kind != MH_FACE_SINGULAR) {
-    for (size_t idx = lane; idx < TT; idx += 32) {
-      const int j = (int)(idx / t), i = (int)(idx - (size_t)j * t);  // (i, j) column-major
-      const double lij = i >= j ? S[idx] : 0.0;
-      FLf[idx] = lij;
-      // FU = L^T : FU(i, j) = L(j, i)
-      FUf[idx] = i <= j ? S[(size_t)i * t + j] : 0.0;
-    }
-    for (int i = lane; i < t; i += 32) {
-      const double d = S[(size_t)i * t + i];
-      FrL[f * t + i] = 1.0 / d;
-      FrU[f * t + i] = 1.0 / d;
-      Fperm[f * t + i] = i;
-    }
-  } else {
+  if (kind == MH_FACE_SINGULAR) {
     sign = 1.0;
     for (size_t idx = lane; idx < TT; idx += 32) {
       const int i = (int)(idx / t), j = (int)(idx - (size_t)i * t);
@@ -303,21 +271,11 @@ __global__ void face_factor_kernel(const double* __restrict__ Drm, double* __res
     for (int i = lane; i < t; i += 32) dmin = fmin(dmin, fabs(S[(size_t)i * t + i]));
     for (int o = 16; o; o >>= 1) dmin = fmin(dmin, __shfl_xor_sync(kFull, dmin, o));
     kind = (dmin < 1e-13 * fmax(dmax, 1e-300)) ? MH_FACE_SINGULAR : MH_FACE_LU;
-    for (size_t idx = lane; idx < TT; idx += 32) {
-      const int j = (int)(idx / t), i = (int)(idx - (size_t)j * t);
-      FLf[idx] = i > j ? S[idx] : (i == j ? 1.0 : 0.0);
-      FUf[idx] = i <= j ? S[idx] : 0.0;
-    }
-    for (int i = lane; i < t; i += 32) {
-      FrL[f * t + i] = 1.0;
-      FrU[f * t + i] = 1.0 / S[(size_t)i * t + i];
-      Fperm[f * t + i] = pm[i];
-    }
   }
-  if (lane == 0) {
-    Fsign[f] = sign;
-    Fkind[f] = (int8_t)kind;
-  }
+  __syncwarp();
+  if (kind != MH_FACE_SINGULAR)
+    warp_inverse(S, pm, t, kind != MH_FACE_LU, sign, scratch, Dinv + f * TT, lane);
+  if (lane == 0) Fkind[f] = (int8_t)kind;
 }
 
 __global__ void transpose_batched_kernel(const double* __restrict__ in, double* __restrict__ out,
@@ -347,12 +305,7 @@ FaceArgs make_args(mh_system* s, const double* in, double* out) {
   a.V = s->V.p;
   a.uhat = in;
   a.out = out;
-  a.FL = s->FL.p;
-  a.FU = s->FU.p;
-  a.FrL = s->FrL.p;
-  a.FrU = s->FrU.p;
-  a.Fperm = s->Fperm.p;
-  a.Fsign = s->Fsign.p;
+  a.Dinv = s->Dinv.p;
   a.F = s->F;
   a.t = s->t;
   return a;
@@ -379,7 +332,7 @@ int launch_transpose_batched(cudaStream_t st, const double* in, double* out, int
 int launch_face_factor(mh_system* s, const double* Drm) {
   if (s->F == 0) return MH_OK;
   const int t = s->t;
-  const size_t per = ((size_t)t * t + 64) * sizeof(double);
+  const size_t per = ((size_t)t * t + 64 + 32 * (size_t)t) * sizeof(double);
   int wpb = (int)((48 * 1024) / per);
   if (wpb < 1) wpb = 1;
   if (wpb > 8) wpb = 8;
@@ -393,9 +346,8 @@ int launch_face_factor(mh_system* s, const double* Drm) {
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   }
   const unsigned grid = (unsigned)((s->F + wpb - 1) / wpb);
-  face_factor_kernel<<<grid, wpb * 32, smem, s->stream>>>(Drm, s->D.p, s->FL.p, s->FU.p, s->FrL.p,
-                                                          s->FrU.p, s->Fperm.p, s->Fsign.p,
-                                                          s->Fkind.p, s->F, t, wpb);
+  face_factor_kernel<<<grid, wpb * 32, smem, s->stream>>>(Drm, s->D.p, s->Dinv.p, s->Fkind.p,
+                                                          s->F, t, wpb);
   MH_CHECK_CUDA(cudaGetLastError());
   return MH_OK;
 }

@@ -109,10 +109,7 @@ struct mh_system {
   mh::DBuf<double> D;      // F*t*t  column-major face blocks
   mh::DBuf<double> Draw;   // F*t*t  row-major face blocks as uploaded (factor input)
   mh::DBuf<double> Rhat;   // F*t
-  mh::DBuf<double> FL, FU; // F*t*t  face factors, column-major (lower / upper)
-  mh::DBuf<double> FrL, FrU;  // F*t reciprocal diagonals
-  mh::DBuf<int32_t> Fperm; // F*t
-  mh::DBuf<double> Fsign;  // F
+  mh::DBuf<double> Dinv;   // F*t*t  D_f^-1 column-major (sign folded in)
   mh::DBuf<int8_t> Fkind;  // F
   mh::DBuf<double> V;      // (N*nfe + extra)*t  element slot contributions
   mh::DBuf<double> tmp;    // F*t scratch
