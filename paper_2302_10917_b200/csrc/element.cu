@@ -36,12 +36,6 @@ namespace {
 
 constexpr int kWPB = 4;                 // consumer warps (macros in flight) per CTA
 constexpr int kThreads = (kWPB + 1) * 32;  // + one producer warp
-constexpr int kRingD = 2048;            // doubles per consumer ring (16 KB)
-constexpr int kChunk = kStreamChunk;    // doubles per bulk-copy chunk (4 KB)
-constexpr int kS = kRingD / kChunk;
-using PipeT = Pipe<kRingD, kChunk, kWPB>;
-using ConsT = Consumer<kRingD, kChunk>;
-constexpr uint32_t kM = kRingD - 1;
 
 struct ElemArgs {
   const int32_t* elem_ufac;
@@ -60,38 +54,44 @@ struct ElemArgs {
   int c_is_bt;
 };
 
-// 32 per-lane partial sums -> lane l holds the full sum of partial l
-// (butterfly transpose-reduce: 31 shuffles for 32 sums).
-__device__ __forceinline__ double transpose_reduce32(double (&p)[32], int lane) {
+// 8 per-lane partial sums -> the full sum of partial (lane >> 2) & 7, held by
+// the 4 lanes with that value of bits 2..4 (3 transpose stages + 2 reductions:
+// 9 shuffles per 8 sums, 8 live registers instead of 32)
+__device__ __forceinline__ double transpose_reduce8(double (&p)[8], int lane) {
 #pragma unroll
-  for (int w = 16; w >= 1; w >>= 1) {
-    const bool upper = (lane & w) != 0;
+  for (int w = 4, bit = 16; w >= 1; w >>= 1, bit >>= 1) {
+    const bool upper = (lane & bit) != 0;
 #pragma unroll
     for (int q = 0; q < w; ++q) {
       const double send = upper ? p[q] : p[q + w];
       const double keep = upper ? p[q + w] : p[q];
-      p[q] = keep + __shfl_xor_sync(kFull, send, w);
+      p[q] = keep + __shfl_xor_sync(kFull, send, bit);
     }
   }
-  return p[0];
+  double v = p[0];
+  v += __shfl_xor_sync(kFull, v, 2);
+  v += __shfl_xor_sync(kFull, v, 1);
+  return v;
 }
 
+template <int RING>
 __device__ __forceinline__ bool no_wrap(uint32_t lo, uint32_t span) {
-  return (lo & kM) + span <= (uint32_t)kRingD;
+  return (lo & (RING - 1)) + span <= (uint32_t)RING;
 }
 
 // x_i += sum over NR rows c of op.B^T[c][perm_i] * ue_c, rows at stream p, p+Q, ...
-template <int R, int NR, bool WRAP, bool PERM>
+template <int R, int NR, int RING, bool WRAP, bool PERM>
 __device__ __forceinline__ void gemv_rows(double (&acc)[R], const double* ring, uint32_t p, int Q,
                                           const double* su, const int (&pr)[R], int lane) {
+  constexpr uint32_t M = RING - 1;
 #pragma unroll
   for (int u = 0; u < NR; ++u) {
     const double uc = su[u];
-    const double* cb = ring + (p & kM);
+    const double* cb = ring + (p & M);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int i = PERM ? pr[r] : lane + 32 * r;
-      const double b = WRAP ? ring[(p + (uint32_t)i) & kM] : cb[i];
+      const double b = WRAP ? ring[(p + (uint32_t)i) & M] : cb[i];
       if (lane + 32 * r < Q) acc[r] = fma(b, uc, acc[r]);
     }
     p += Q;
@@ -100,20 +100,21 @@ __device__ __forceinline__ void gemv_rows(double (&acc)[R], const double* ring, 
 
 // forward substitution over NC packed L columns j0.. (JB = j0 / 32 is a
 // compile-time constant once the caller's block loop is unrolled)
-template <int R, int NC, bool WRAP>
+template <int R, int NC, int RING, bool WRAP>
 __device__ __forceinline__ void fwd_cols(double (&y)[R], const double* ring, uint32_t p, int JB,
                                          int j0, int Q, int lane) {
+  constexpr uint32_t M = RING - 1;
   const int jj0 = j0 & 31;
 #pragma unroll
   for (int u = 0; u < NC; ++u) {
     const int j = j0 + u;
     const uint32_t q0 = p - (uint32_t)(j + 1);  // stream position of "row 0"
     const double yj = __shfl_sync(kFull, y[JB], jj0 + u);
-    const double* cb = ring + (q0 & kM);
+    const double* cb = ring + (q0 & M);
 #pragma unroll
     for (int r = JB; r < R; ++r) {
       const int i = lane + 32 * r;
-      const double l = WRAP ? ring[(q0 + (uint32_t)i) & kM] : cb[i];
+      const double l = WRAP ? ring[(q0 + (uint32_t)i) & M] : cb[i];
       if (r > JB || lane > jj0 + u) y[r] = fma(-l, yj, y[r]);
     }
     p += (uint32_t)(Q - 1 - j);
@@ -121,21 +122,22 @@ __device__ __forceinline__ void fwd_cols(double (&y)[R], const double* ring, uin
 }
 
 // back substitution over NC packed U columns j0, j0-1, .. (descending)
-template <int R, int NC, bool WRAP>
+template <int R, int NC, int RING, bool WRAP>
 __device__ __forceinline__ void bwd_cols(double (&y)[R], const double (&dr)[R],
                                          const double* ring, uint32_t p, int JB, int j0,
                                          int lane) {
+  constexpr uint32_t M = RING - 1;
   const int jj0 = j0 & 31;
 #pragma unroll
   for (int u = 0; u < NC; ++u) {
     const int j = j0 - u;
     if (lane == jj0 - u) y[JB] *= dr[JB];
     const double yj = __shfl_sync(kFull, y[JB], jj0 - u);
-    const double* cb = ring + (p & kM);
+    const double* cb = ring + (p & M);
 #pragma unroll
     for (int r = 0; r <= JB; ++r) {
       const int i = lane + 32 * r;
-      const double uv = WRAP ? ring[(p + (uint32_t)i) & kM] : cb[i];
+      const double uv = WRAP ? ring[(p + (uint32_t)i) & M] : cb[i];
       if (r < JB || lane < jj0 - u) y[r] = fma(-uv, yj, y[r]);
     }
     p += (uint32_t)j;
@@ -143,32 +145,36 @@ __device__ __forceinline__ void bwd_cols(double (&y)[R], const double (&dr)[R],
 }
 
 // partial dot product of one op.C row with y
-template <int R, bool WRAP>
+template <int R, int RING, bool WRAP>
 __device__ __forceinline__ double dot_row(const double (&y)[R], const double* ring, uint32_t p,
                                           int Q, int lane) {
+  constexpr uint32_t M = RING - 1;
   double acc = 0.0;
-  const double* cb = ring + (p & kM);
+  const double* cb = ring + (p & M);
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int i = lane + 32 * r;
-    const double c = WRAP ? ring[(p + (uint32_t)i) & kM] : cb[i];
+    const double c = WRAP ? ring[(p + (uint32_t)i) & M] : cb[i];
     if (i < Q) acc = fma(c, y[r], acc);
   }
   return acc;
 }
 
-template <int R, int MODE>
+template <int R, int MODE, int RING, int CH>
 __global__ void __launch_bounds__(kThreads, 3)
 element_kernel(ElemArgs a) {
+  constexpr int S = RING / CH;
+  using PipeT = Pipe<RING, CH, kWPB>;
+  using ConsT = Consumer<RING, CH>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ Segment segs[4];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int Q = a.Q, nc = a.nc, t = a.t;
-  const int nchB = (int)(a.ldB / kChunk), nchL = (int)(a.ldL / kChunk);
+  const int nchB = (int)(a.ldB / CH), nchL = (int)(a.ldL / CH);
   double* rings = reinterpret_cast<double*>(smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(rings + (size_t)kWPB * kRingD);
-  uint64_t* empty = full + kWPB * kS;
-  double* su_all = reinterpret_cast<double*>(empty + kWPB * kS);
+  uint64_t* full = reinterpret_cast<uint64_t*>(rings + (size_t)kWPB * RING);
+  uint64_t* empty = full + kWPB * S;
+  double* su_all = reinterpret_cast<double*>(empty + kWPB * S);
   const int nseg = (MODE != kRhs ? 1 : 0) + 2 + (MODE != kRecon ? 1 : 0);
   if (threadIdx.x == 0) {
     int n = 0;
@@ -176,7 +182,7 @@ element_kernel(ElemArgs a) {
     segs[n++] = Segment{a.Lp, a.ldL, nchL, 0};
     segs[n++] = Segment{a.Up, a.ldL, nchL, 0};
     if (MODE != kRecon) segs[n++] = Segment{a.Cm, a.ldB, nchB, 0};
-    for (int i = 0; i < 2 * kWPB * kS; ++i) mbar_init(&full[i], 1);  // full + empty
+    for (int i = 0; i < 2 * kWPB * S; ++i) mbar_init(&full[i], 1);  // full + empty
     fence_mbar_init();
   }
   __syncthreads();  // the only CTA-wide barrier
@@ -186,11 +192,11 @@ element_kernel(ElemArgs a) {
       PipeT::produce(rings, full, empty, segs, nseg, (int64_t)blockIdx.x * kWPB, W, a.N, kWPB);
     return;
   }
-  const double* ring = rings + (size_t)w * kRingD;
+  const double* ring = rings + (size_t)w * RING;
   double* su = su_all + (size_t)w * ((nc + 3) & ~3);
   ConsT cs;
-  cs.full = full + w * kS;
-  cs.empty = empty + w * kS;
+  cs.full = full + w * S;
+  cs.empty = empty + w * S;
   const uint32_t offL = (MODE != kRhs) ? (uint32_t)a.ldB : 0u;
   const uint32_t offU = offL + (uint32_t)a.ldL;
   const uint32_t offC = offU + (uint32_t)a.ldL;
@@ -230,16 +236,15 @@ element_kernel(ElemArgs a) {
       int c = 0;
       for (; c + 4 <= nc; c += 4, p += 4u * (uint32_t)Q) {  // step 1: x = B ue
         cs.window(p, p + 4u * Q, lane);
-        if (no_wrap(p, 4u * Q + 32u * R)) {
-          if (has_perm) gemv_rows<R, 4, false, true>(acc, ring, p, Q, su + c, pr, lane);
-          else gemv_rows<R, 4, false, false>(acc, ring, p, Q, su + c, pr, lane);
+        if (!has_perm && no_wrap<RING>(p, 4u * Q + 32u * R)) {
+          gemv_rows<R, 4, RING, false, false>(acc, ring, p, Q, su + c, pr, lane);
         } else {
-          gemv_rows<R, 4, true, true>(acc, ring, p, Q, su + c, pr, lane);
+          gemv_rows<R, 4, RING, true, true>(acc, ring, p, Q, su + c, pr, lane);
         }
       }
       for (; c < nc; ++c, p += (uint32_t)Q) {
         cs.window(p, p + Q, lane);
-        gemv_rows<R, 1, true, true>(acc, ring, p, Q, su + c, pr, lane);
+        gemv_rows<R, 1, RING, true, true>(acc, ring, p, Q, su + c, pr, lane);
       }
       __syncwarp();  // su is rewritten by the next macro
 #pragma unroll
@@ -259,16 +264,21 @@ element_kernel(ElemArgs a) {
         for (; j0 + 4 <= jend; j0 += 4) {
           const uint32_t span = (uint32_t)(4 * (Q - 1 - j0) - 6);
           cs.window(p, p + span, lane);
-          if (no_wrap(p - (uint32_t)(j0 + 1), span + (uint32_t)(j0 + 1) + 32u * R + 8u))
-            fwd_cols<R, 4, false>(y, ring, p, jb, j0, Q, lane);
-          else
-            fwd_cols<R, 4, true>(y, ring, p, jb, j0, Q, lane);
-          p += span;
+          if (no_wrap<RING>(p - (uint32_t)(j0 + 1), span + (uint32_t)(j0 + 1) + 32u * R + 8u)) {
+            fwd_cols<R, 4, RING, false>(y, ring, p, jb, j0, Q, lane);
+            p += span;
+          } else {
+#pragma unroll 1
+            for (int u = 0; u < 4; ++u) {  // rare: the group wraps around the ring end
+              fwd_cols<R, 1, RING, true>(y, ring, p, jb, j0 + u, Q, lane);
+              p += (uint32_t)(Q - 1 - (j0 + u));
+            }
+          }
         }
         for (; j0 < jend; ++j0) {
           const uint32_t span = (uint32_t)(Q - 1 - j0);
           cs.window(p, p + span, lane);
-          fwd_cols<R, 1, true>(y, ring, p, jb, j0, Q, lane);
+          fwd_cols<R, 1, RING, true>(y, ring, p, jb, j0, Q, lane);
           p += span;
         }
       }
@@ -283,15 +293,20 @@ element_kernel(ElemArgs a) {
         for (; j0 - 3 >= jb * 32; j0 -= 4) {
           const uint32_t span = (uint32_t)(4 * j0 - 6);
           cs.window(p, p + span, lane);
-          if (no_wrap(p, span + 32u * R + 8u))
-            bwd_cols<R, 4, false>(y, dr, ring, p, jb, j0, lane);
-          else
-            bwd_cols<R, 4, true>(y, dr, ring, p, jb, j0, lane);
-          p += span;
+          if (no_wrap<RING>(p, span + 32u * R + 8u)) {
+            bwd_cols<R, 4, RING, false>(y, dr, ring, p, jb, j0, lane);
+            p += span;
+          } else {
+#pragma unroll 1
+            for (int u = 0; u < 4; ++u) {
+              bwd_cols<R, 1, RING, true>(y, dr, ring, p, jb, j0 - u, lane);
+              p += (uint32_t)(j0 - u);
+            }
+          }
         }
         for (; j0 >= jb * 32; --j0) {
           cs.window(p, p + j0, lane);
-          bwd_cols<R, 1, true>(y, dr, ring, p, jb, j0, lane);
+          bwd_cols<R, 1, RING, true>(y, dr, ring, p, jb, j0, lane);
           p += (uint32_t)j0;
         }
       }
@@ -306,21 +321,23 @@ element_kernel(ElemArgs a) {
       continue;
     }
 
-    // step 3: v_c = sum_i C[c][i] y_i, 32 rows per transpose-reduce
+    // step 3: v_c = sum_i C[c][i] y_i, 8 rows per transpose-reduce
     uint32_t p = base + offC;
-    for (int c0 = 0; c0 < nc; c0 += 32) {
-      double pp[32];
-      const int nrow = min(32, nc - c0);
+    for (int c0 = 0; c0 < nc; c0 += 8) {
+      double pp[8];
+      const int nrow = min(8, nc - c0);
 #pragma unroll
-      for (int q0 = 0; q0 < 32; q0 += 4) {
+      for (int q0 = 0; q0 < 8; q0 += 4) {
         if (q0 + 4 <= nrow) {
           cs.window(p, p + 4u * Q, lane);
-          if (no_wrap(p, 4u * Q + 32u * R)) {
+          if (no_wrap<RING>(p, 4u * Q + 32u * R)) {
 #pragma unroll
-            for (int u = 0; u < 4; ++u) pp[q0 + u] = dot_row<R, false>(y, ring, p + u * Q, Q, lane);
+            for (int u = 0; u < 4; ++u)
+              pp[q0 + u] = dot_row<R, RING, false>(y, ring, p + u * Q, Q, lane);
           } else {
 #pragma unroll
-            for (int u = 0; u < 4; ++u) pp[q0 + u] = dot_row<R, true>(y, ring, p + u * Q, Q, lane);
+            for (int u = 0; u < 4; ++u)
+              pp[q0 + u] = dot_row<R, RING, true>(y, ring, p + u * Q, Q, lane);
           }
           p += 4u * Q;
         } else {
@@ -328,7 +345,7 @@ element_kernel(ElemArgs a) {
           for (int u = 0; u < 4; ++u) {
             if (q0 + u < nrow) {
               cs.window(p, p + Q, lane);
-              pp[q0 + u] = dot_row<R, true>(y, ring, p, Q, lane);
+              pp[q0 + u] = dot_row<R, RING, true>(y, ring, p, Q, lane);
               p += Q;
             } else {
               pp[q0 + u] = 0.0;
@@ -336,21 +353,29 @@ element_kernel(ElemArgs a) {
           }
         }
       }
-      const double v = transpose_reduce32(pp, lane);
-      if (c0 + lane < nc) a.out[e * nc + c0 + lane] = v;
+      const double v = transpose_reduce8(pp, lane);
+      const int row = (lane >> 2) & 7;
+      if ((lane & 3) == 0 && row < nrow) a.out[e * nc + c0 + row] = v;
     }
   }
 }
 
+template <int RING, int CH>
 size_t smem_bytes(int nc) {
-  return (size_t)kWPB * kRingD * sizeof(double) + (size_t)2 * kWPB * kS * sizeof(uint64_t) +
+  return (size_t)kWPB * RING * sizeof(double) + (size_t)2 * kWPB * (RING / CH) * sizeof(uint64_t) +
          (size_t)kWPB * ((nc + 3) & ~3) * sizeof(double);
 }
 
 template <int R, int MODE>
 int launch_rm(mh_system* s, const ElemArgs& a) {
-  const size_t smem = smem_bytes(s->nc);
-  auto kern = element_kernel<R, MODE>;
+  // 16 KB rings of 4 KB chunks (3 CTAs = 12 consumer warps per SM); measured
+  // faster than 8 KB rings of 2 KB chunks at 4 CTAs per SM (fewer waits, more
+  // bytes in flight per warp)
+  constexpr int RING = 2048;
+  constexpr int CH = 512;
+  static_assert(kStreamChunk % CH == 0, "HBM padding must be a multiple of the ring chunk");
+  const size_t smem = smem_bytes<RING, CH>(s->nc);
+  auto kern = element_kernel<R, MODE, RING, CH>;
   MH_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   MH_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));

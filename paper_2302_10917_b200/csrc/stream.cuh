@@ -169,15 +169,25 @@ struct Consumer {
   uint64_t* empty;
   uint32_t released = 0, waited = 0, ready_end = 0;
 
-  // make stream positions [.., b) readable, releasing every chunk before a
+  // make stream positions [.., b) readable, releasing every chunk before a.
+  // Chunks are retired strictly in order and only after their data has
+  // landed: a chunk the consumer skipped (segment padding) is waited for
+  // before its slot is handed back, so the full/empty barrier phases of a
+  // slot can never run two uses apart.
   __device__ __forceinline__ void window(uint32_t a, uint32_t b, int lane) {
     if (b <= ready_end) return;
     const uint32_t rel = a / CH;
     if (rel > released) {
       __syncwarp();  // the whole warp is done with those slots
-      if (lane == 0)
-        for (uint32_t c = released; c < rel; ++c) mbar_arrive(&empty[c % S]);
-      released = rel;
+      while (released < rel) {
+        if (waited <= released) {
+          while (!mbar_try_wait(&full[released % S], (released / S) & 1u)) {
+          }
+          waited = released + 1;
+        }
+        if (lane == 0) mbar_arrive(&empty[released % S]);
+        ++released;
+      }
     }
     while (waited * CH < b) {
       const uint32_t c = waited;
