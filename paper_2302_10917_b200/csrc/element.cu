@@ -76,22 +76,21 @@ __device__ __forceinline__ double transpose_reduce8(double (&p)[8], int lane) {
 
 template <int RING>
 __device__ __forceinline__ bool no_wrap(uint32_t lo, uint32_t span) {
-  return (lo & (RING - 1)) + span <= (uint32_t)RING;
+  return rmod<RING>(lo) + span <= (uint32_t)RING;
 }
 
 // x_i += sum over NR rows c of op.B^T[c][perm_i] * ue_c, rows at stream p, p+Q, ...
 template <int R, int NR, int RING, bool WRAP, bool PERM>
 __device__ __forceinline__ void gemv_rows(double (&acc)[R], const double* ring, uint32_t p, int Q,
                                           const double* su, const int (&pr)[R], int lane) {
-  constexpr uint32_t M = RING - 1;
 #pragma unroll
   for (int u = 0; u < NR; ++u) {
     const double uc = su[u];
-    const double* cb = ring + (p & M);
+    const double* cb = ring + rmod<RING>(p);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int i = PERM ? pr[r] : lane + 32 * r;
-      const double b = WRAP ? ring[(p + (uint32_t)i) & M] : cb[i];
+      const double b = WRAP ? ring[rmod<RING>(p + (uint32_t)i)] : cb[i];
       if (lane + 32 * r < Q) acc[r] = fma(b, uc, acc[r]);
     }
     p += Q;
@@ -103,18 +102,17 @@ __device__ __forceinline__ void gemv_rows(double (&acc)[R], const double* ring, 
 template <int R, int NC, int RING, bool WRAP>
 __device__ __forceinline__ void fwd_cols(double (&y)[R], const double* ring, uint32_t p, int JB,
                                          int j0, int Q, int lane) {
-  constexpr uint32_t M = RING - 1;
   const int jj0 = j0 & 31;
 #pragma unroll
   for (int u = 0; u < NC; ++u) {
     const int j = j0 + u;
     const uint32_t q0 = p - (uint32_t)(j + 1);  // stream position of "row 0"
     const double yj = __shfl_sync(kFull, y[JB], jj0 + u);
-    const double* cb = ring + (q0 & M);
+    const double* cb = ring + rmod<RING>(q0);
 #pragma unroll
     for (int r = JB; r < R; ++r) {
       const int i = lane + 32 * r;
-      const double l = WRAP ? ring[(q0 + (uint32_t)i) & M] : cb[i];
+      const double l = WRAP ? ring[rmod<RING>(q0 + (uint32_t)i)] : cb[i];
       if (r > JB || lane > jj0 + u) y[r] = fma(-l, yj, y[r]);
     }
     p += (uint32_t)(Q - 1 - j);
@@ -126,18 +124,17 @@ template <int R, int NC, int RING, bool WRAP>
 __device__ __forceinline__ void bwd_cols(double (&y)[R], const double (&dr)[R],
                                          const double* ring, uint32_t p, int JB, int j0,
                                          int lane) {
-  constexpr uint32_t M = RING - 1;
   const int jj0 = j0 & 31;
 #pragma unroll
   for (int u = 0; u < NC; ++u) {
     const int j = j0 - u;
     if (lane == jj0 - u) y[JB] *= dr[JB];
     const double yj = __shfl_sync(kFull, y[JB], jj0 - u);
-    const double* cb = ring + (p & M);
+    const double* cb = ring + rmod<RING>(p);
 #pragma unroll
     for (int r = 0; r <= JB; ++r) {
       const int i = lane + 32 * r;
-      const double uv = WRAP ? ring[(p + (uint32_t)i) & M] : cb[i];
+      const double uv = WRAP ? ring[rmod<RING>(p + (uint32_t)i)] : cb[i];
       if (r < JB || lane < jj0 - u) y[r] = fma(-uv, yj, y[r]);
     }
     p += (uint32_t)j;
@@ -148,13 +145,12 @@ __device__ __forceinline__ void bwd_cols(double (&y)[R], const double (&dr)[R],
 template <int R, int RING, bool WRAP>
 __device__ __forceinline__ double dot_row(const double (&y)[R], const double* ring, uint32_t p,
                                           int Q, int lane) {
-  constexpr uint32_t M = RING - 1;
   double acc = 0.0;
-  const double* cb = ring + (p & M);
+  const double* cb = ring + rmod<RING>(p);
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int i = lane + 32 * r;
-    const double c = WRAP ? ring[(p + (uint32_t)i) & M] : cb[i];
+    const double c = WRAP ? ring[rmod<RING>(p + (uint32_t)i)] : cb[i];
     if (i < Q) acc = fma(c, y[r], acc);
   }
   return acc;
@@ -368,9 +364,9 @@ size_t smem_bytes(int nc) {
 
 template <int R, int MODE>
 int launch_rm(mh_system* s, const ElemArgs& a) {
-  // 16 KB rings of 4 KB chunks (3 CTAs = 12 consumer warps per SM); measured
-  // faster than 8 KB rings of 2 KB chunks at 4 CTAs per SM (fewer waits, more
-  // bytes in flight per warp)
+  // 16 KB rings of four 4 KB chunks, 3 CTAs = 12 consumer warps per SM.
+  // Measured alternatives at c2: 8 KB rings of 2 KB chunks at 4 CTAs/SM
+  // -13%, 12 KB rings of three 4 KB chunks at 4 CTAs/SM -1.5%.
   constexpr int RING = 2048;
   constexpr int CH = 512;
   static_assert(kStreamChunk % CH == 0, "HBM padding must be a multiple of the ring chunk");

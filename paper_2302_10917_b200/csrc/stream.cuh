@@ -83,6 +83,12 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// ring offset of a stream position (RING need not be a power of two)
+template <int RING>
+__device__ __forceinline__ uint32_t rmod(uint32_t x) {
+  return (RING & (RING - 1)) == 0 ? (x & (RING - 1)) : (x % RING);
+}
+
 // Per-macro segment of the stream.  Every segment is padded to a multiple
 // of the chunk size CH in HBM, so each chunk is exactly one bulk copy.
 struct Segment {
@@ -100,8 +106,6 @@ struct Segment {
 template <int RING, int CH, int NCONS>
 struct Pipe {
   static constexpr int S = RING / CH;
-  static constexpr uint32_t M = RING - 1;
-  static_assert((RING & (RING - 1)) == 0, "ring must be a power of two");
   static_assert(RING % CH == 0 && S >= 2, "ring must hold >= 2 chunks");
 
   // producer warp, lane 0: feed the NCONS consumer streams until done
