@@ -370,6 +370,219 @@ __global__ void __launch_bounds__(NW * 32, 512 / (NW * 32)) lu_reg_kernel(LuArgs
   }
 }
 
+// ---------------------------------------------------------------------------
+// Blocked right-looking variant with fp64 tensor-core trailing updates.
+//
+// The block (padded to QP = 32 RW rows/columns, zeros outside Q) lives in
+// shared memory, row-major with leading dimension LD (LD % 16 == 4 keeps the
+// DMMA fragment loads bank-conflict free).  Per panel of 8 columns:
+//   1. warp 0 factors the panel (rows >= c0) in registers: idamax via REDUX on
+//      the bit pattern of |a_ik| (first index on ties), LAPACK row exchange,
+//      reciprocal scaling, rank-1 update of the remaining panel columns;
+//   2. all threads apply the panel's row exchanges to the other columns and
+//      form U12 = L11^-1 A12 (one thread per trailing column);
+//   3. the trailing block A22 -= L21 U12 is updated 8x8 tile by tile with
+//      mma.sync.m8n8k4.f64 (SASS DMMA), two k-steps per tile.
+// Three CTA barriers per 8 columns instead of one per column.
+template <int RW>
+__device__ __forceinline__ double pick_r(const double (&col)[RW], int a_sel) {
+  double v = col[0];
+#pragma unroll
+  for (int a = 1; a < RW; ++a) v = osel(a == a_sel, col[a], v);
+  return v;
+}
+
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <int RW, int LD>
+__global__ void __launch_bounds__(256) lu_dmma_kernel(LuArgs g) {
+  constexpr int QP = 32 * RW;
+  constexpr int NT = 256, NW = 8;
+  extern __shared__ double Ws[];  // QP x LD row-major
+  __shared__ int s_pv[8];
+  __shared__ int s_perm[QP];
+  __shared__ double red[NW];
+  static_assert(LD % 16 == 4 && LD >= QP, "LD");
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t e = blockIdx.x;
+  const int Q = g.Q;
+  const double* __restrict__ Ae = g.A + e * (int64_t)Q * Q;
+
+  double amax = 0.0;
+  for (int idx = tid; idx < QP * QP; idx += NT) {
+    const int i = idx / QP, j = idx - i * QP;
+    const double v = (i < Q && j < Q) ? __ldg(Ae + (int64_t)i * Q + j) : 0.0;
+    Ws[i * LD + j] = v;
+    amax = fmax(amax, fabs(v));
+  }
+  for (int i = tid; i < QP; i += NT) s_perm[i] = i;
+  for (int o = 16; o; o >>= 1) amax = fmax(amax, __shfl_xor_sync(kFull, amax, o));
+  if (lane == 0) red[warp] = amax;
+  __syncthreads();
+  amax = 0.0;
+#pragma unroll
+  for (int i = 0; i < NW; ++i) amax = fmax(amax, red[i]);
+  double dmin = DBL_MAX;
+  const int npanel = (Q + 7) / 8;
+
+  for (int pnl = 0; pnl < npanel; ++pnl) {
+    const int c0 = pnl * 8;
+    // ---- 1. panel factorisation (warp 0, rows c0.., columns c0..c0+7)
+    if (warp == 0) {
+      double P[8][RW];
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj)
+#pragma unroll
+        for (int a = 0; a < RW; ++a) {
+          const int i = lane + 32 * a;
+          P[jj][a] = (i >= c0) ? Ws[i * LD + c0 + jj] : 0.0;
+        }
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) {
+        const int k = c0 + jj;
+        if (k >= Q) break;
+        // idamax over rows k..Q-1 of panel column jj
+        uint64_t key[RW];
+        uint64_t best = 0;
+#pragma unroll
+        for (int a = 0; a < RW; ++a) {
+          const int i = lane + 32 * a;
+          key[a] = (i >= k && i < Q) ? (uint64_t)__double_as_longlong(fabs(P[jj][a])) + 1ull : 0ull;
+          best = key[a] > best ? key[a] : best;
+        }
+        const unsigned hi = (unsigned)(best >> 32);
+        const unsigned mhi = __reduce_max_sync(kFull, hi);
+        const unsigned lo = hi == mhi ? (unsigned)(best & 0xffffffffu) : 0u;
+        const unsigned mlo = __reduce_max_sync(kFull, lo);
+        const uint64_t mk = ((uint64_t)mhi << 32) | mlo;
+        int p = k;
+#pragma unroll
+        for (int a = RW - 1; a >= 0; --a) {
+          const unsigned m = __ballot_sync(kFull, key[a] == mk);
+          if (m) p = 32 * a + __ffs(m) - 1;
+        }
+        const int ak = k >> 5, lk = k & 31, ap = p >> 5, lp = p & 31;
+        const double pv = __shfl_sync(kFull, pick_r<RW>(P[jj], ap), lp);
+        if (p != k && pv != 0.0) {  // exchange rows k and p inside the panel
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const double vk = __shfl_sync(kFull, pick_r<RW>(P[c], ak), lk);
+            const double vp = __shfl_sync(kFull, pick_r<RW>(P[c], ap), lp);
+#pragma unroll
+            for (int a = 0; a < RW; ++a) {
+              P[c][a] = osel(a == ak && lane == lk, vp, P[c][a]);
+              P[c][a] = osel(a == ap && lane == lp, vk, P[c][a]);
+            }
+          }
+        }
+        const bool big = fabs(pv) >= DBL_MIN;
+        const double rcp = 1.0 / pv;
+#pragma unroll
+        for (int a = 0; a < RW; ++a) {
+          const int i = lane + 32 * a;
+          if (i > k && i < Q && pv != 0.0) P[jj][a] = big ? P[jj][a] * rcp : P[jj][a] / pv;
+        }
+#pragma unroll
+        for (int c = jj + 1; c < 8; ++c) {  // rank-1 update inside the panel
+          const double u = __shfl_sync(kFull, pick_r<RW>(P[c], ak), lk);
+#pragma unroll
+          for (int a = 0; a < RW; ++a)
+            if (lane + 32 * a > k) P[c][a] = fma(-P[jj][a], u, P[c][a]);
+        }
+        if (lane == 0) {
+          const int pe = (pv != 0.0) ? p : k;
+          s_pv[jj] = pe;
+          g.piv[e * Q + k] = p;
+          if (pe != k) {
+            const int tmp = s_perm[k];
+            s_perm[k] = s_perm[pe];
+            s_perm[pe] = tmp;
+          }
+          dmin = fmin(dmin, fabs(pv));
+        }
+      }
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj)
+#pragma unroll
+        for (int a = 0; a < RW; ++a) {
+          const int i = lane + 32 * a;
+          if (i >= c0) Ws[i * LD + c0 + jj] = P[jj][a];
+        }
+    }
+    __syncthreads();
+    // ---- 2. row exchanges outside the panel + U12 = L11^-1 A12
+    const int ncolp = min(8, Q - c0);
+    for (int j = tid; j < QP; j += NT) {
+      if (j >= c0 && j < c0 + 8) continue;
+      for (int jj = 0; jj < ncolp; ++jj) {
+        const int k = c0 + jj, p = s_pv[jj];
+        if (p != k) {
+          const double t = Ws[k * LD + j];
+          Ws[k * LD + j] = Ws[p * LD + j];
+          Ws[p * LD + j] = t;
+        }
+      }
+      if (j >= c0 + 8) {
+        double u[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) u[r] = Ws[(c0 + r) * LD + j];
+#pragma unroll
+        for (int r = 1; r < 8; ++r)
+#pragma unroll
+          for (int m = 0; m < r; ++m) u[r] = fma(-Ws[(c0 + r) * LD + c0 + m], u[m], u[r]);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) Ws[(c0 + r) * LD + j] = u[r];
+      }
+    }
+    __syncthreads();
+    // ---- 3. A22 -= L21 U12 on 8x8 tiles with DMMA
+    const int t0 = pnl + 1, nt = QP / 8 - t0;
+    if (nt > 0) {
+      const int r = lane >> 2, q = lane & 3;
+      for (int tile = warp; tile < nt * nt; tile += NW) {
+        const int ti = t0 + tile / nt, tj = t0 + tile % nt;
+        const int row = ti * 8 + r, col = tj * 8 + 2 * q;
+        double d0 = Ws[row * LD + col], d1 = Ws[row * LD + col + 1];
+#pragma unroll
+        for (int k0 = 0; k0 < 8; k0 += 4) {
+          const double av = -Ws[row * LD + c0 + k0 + q];           // A: row r, k = q
+          const double bv = Ws[(c0 + k0 + q) * LD + tj * 8 + r];   // B: k = q, col r
+          dmma_8x8x4(d0, d1, av, bv);
+        }
+        Ws[row * LD + col] = d0;
+        Ws[row * LD + col + 1] = d1;
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- outputs (same packed streams as the other variants)
+  double* Lpe = g.Lp + e * g.ldL;
+  double* Upe = g.Up + e * g.ldL;
+  for (int j = warp; j < Q; j += NW) {
+    const int64_t ol = off_lower(j, Q), ou = off_upper(j, Q);
+    for (int i = lane; i < Q; i += 32) {
+      const double v = Ws[i * LD + j];
+      if (i > j) Lpe[ol + (i - j - 1)] = v;
+      else if (i < j) Upe[ou + i] = v;
+      else {
+        g.udiag[e * Q + i] = v;
+        g.dinv[e * Q + i] = 1.0 / v;
+      }
+    }
+  }
+  for (int64_t i = (int64_t)Q * (Q - 1) / 2 + tid; i < g.ldL; i += NT) {
+    Lpe[i] = 0.0;
+    Upe[i] = 0.0;
+  }
+  for (int i = tid; i < Q; i += NT) g.perm[e * Q + i] = s_perm[i];
+  if (tid == 0) g.stat[e] = (dmin <= 1e-13 * fmax(amax, 1e-300)) ? 1 : 0;
+}
+
 __global__ void unpack_lu_kernel(const double* __restrict__ Lp, const double* __restrict__ Up,
                                  const double* __restrict__ udiag, int64_t ldL, int Q,
                                  int64_t first, int64_t count, double* __restrict__ out) {
@@ -437,8 +650,19 @@ int launch_lu(mh_system* s, float* ms) {
   const int Q = s->Q;
   const unsigned grid = (unsigned)s->N;
   if (Q <= 32) lu_reg_kernel<1, 4, 8><<<grid, 256, 0, s->stream>>>(g);
-  else if (Q <= 64) lu_reg_kernel<2, 8, 8><<<grid, 256, 0, s->stream>>>(g);
-  else if (Q <= 96) lu_reg_kernel<3, 12, 8><<<grid, 256, 0, s->stream>>>(g);
+  else if (Q <= 64) {
+    constexpr int LD = 68;
+    const size_t sm = (size_t)64 * LD * sizeof(double);
+    MH_CHECK_CUDA(cudaFuncSetAttribute(lu_dmma_kernel<2, LD>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    lu_dmma_kernel<2, LD><<<grid, 256, sm, s->stream>>>(g);
+  } else if (Q <= 96) {
+    constexpr int LD = 100;
+    const size_t sm = (size_t)96 * LD * sizeof(double);
+    MH_CHECK_CUDA(cudaFuncSetAttribute(lu_dmma_kernel<3, LD>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    lu_dmma_kernel<3, LD><<<grid, 256, sm, s->stream>>>(g);
+  }
   else if (Q <= 128) lu_reg_kernel<4, 8, 16><<<grid, 512, 0, s->stream>>>(g);
   else {
     if (!use_smem) {

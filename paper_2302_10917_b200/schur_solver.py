@@ -357,29 +357,35 @@ def _dev_vec(sys, n=None):
                        device=f"cuda:{sys.device}")
 
 
-def _run(sys, fn, name, x):
-    """Apply a device op to numpy (host path) or torch CUDA input."""
+def _run(sys, fn, name, x, out=None):
+    """Apply a device op to numpy (host path) or torch CUDA input.  `out`
+    (optional) receives the result -- e.g. a pinned host array."""
     if _is_torch(x):
         if x.dtype != _torch().float64 or not x.is_cuda:
             raise TypeError("device vectors must be float64 CUDA tensors")
         x = x.contiguous()
-        out = _dev_vec(sys)
+        out = _dev_vec(sys) if out is None else out
         check(fn(sys.handle, ptr(x), ptr(out)), name)
         return out
     xh = np.ascontiguousarray(x, dtype=np.float64)
     if xh.shape != (sys.zhat,):
         raise ValueError(f"expected a vector of length {sys.zhat}")
-    out = np.empty(sys.zhat)
+    if out is None:
+        out = np.empty(sys.zhat)
+    elif out.shape != (sys.zhat,) or out.dtype != np.float64 or not out.flags.c_contiguous:
+        raise ValueError("out must be a contiguous float64 vector of length zhat")
     host_fn = {"mh_apply": lib.mh_apply_host, "mh_precond": lib.mh_precond_host}[name]
     check(host_fn(sys.handle, ptr(xh), ptr(out)), name)
     return out
 
 
-def apply_schur(sys: CondensedSystem, uhat):
+def apply_schur(sys: CondensedSystem, uhat, out=None):
     """(D - C A^-1 B) uhat via the fused element kernel + face reduction
-    (schur_solver.py:267-293)."""
+    (schur_solver.py:267-293).  ``out`` is an optional preallocated result
+    (numpy for host input -- pinned memory avoids a staged copy -- or a CUDA
+    tensor for device input); the reference signature is the default."""
     t0 = time.perf_counter()
-    w = _run(sys, lib.mh_apply, "mh_apply", uhat)
+    w = _run(sys, lib.mh_apply, "mh_apply", uhat, out)
     sys.counters["macro_apply"] += sys.N
     sys.counters["face_reduce"] += sys.F
     sys.timings["local"] += time.perf_counter() - t0
