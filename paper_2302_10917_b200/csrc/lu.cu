@@ -382,8 +382,10 @@ __global__ void __launch_bounds__(NW * 32, 512 / (NW * 32)) lu_reg_kernel(LuArgs
 //   2. all threads apply the panel's row exchanges to the other columns and
 //      form U12 = L11^-1 A12 (one thread per trailing column);
 //   3. the trailing block A22 -= L21 U12 is updated 8x8 tile by tile with
-//      mma.sync.m8n8k4.f64 (SASS DMMA), two k-steps per tile.
-// Three CTA barriers per 8 columns instead of one per column.
+//      mma.sync.m8n8k4.f64 (SASS DMMA), two k-steps per tile.  Look-ahead:
+//      warp 0 updates the next panel's tile column first and factors that
+//      panel while warps 1..7 update the rest of the trailing block.
+// Two CTA barriers per 8 columns.
 template <int RW>
 __device__ __forceinline__ double pick_r(const double (&col)[RW], int a_sel) {
   double v = col[0];
@@ -398,9 +400,127 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
                : "d"(a), "d"(b));
 }
 
+// one 8x8 tile of A22 -= L21(rows of ti, panel columns) U12(panel rows, cols of tj)
+template <int LD>
+__device__ __forceinline__ void tile_update(double* Ws, int c0, int ti, int tj, int lane) {
+  const int r = lane >> 2, q = lane & 3;
+  const int row = ti * 8 + r, col = tj * 8 + 2 * q;
+  double d0 = Ws[row * LD + col], d1 = Ws[row * LD + col + 1];
+#pragma unroll
+  for (int k0 = 0; k0 < 8; k0 += 4) {
+    const double av = -Ws[row * LD + c0 + k0 + q];          // A: row r, k = q
+    const double bv = Ws[(c0 + k0 + q) * LD + tj * 8 + r];  // B: k = q, col r
+    dmma_8x8x4(d0, d1, av, bv);
+  }
+  Ws[row * LD + col] = d0;
+  Ws[row * LD + col + 1] = d1;
+}
+
+// Panel factorisation by one warp.  AK = c0 / 32 is static (8 | 32), so the
+// pivot row of every step sits in register block AK of some lane.
+template <int RW, int LD, int AK>
+__device__ __noinline__ double panel_factor(double* Ws, int c0, int Q, int lane, int* s_pv,
+                                            int* s_perm, int* piv) {
+  double P[8][RW];
+#pragma unroll
+  for (int jj = 0; jj < 8; ++jj)
+#pragma unroll
+    for (int a = AK; a < RW; ++a) P[jj][a] = Ws[(lane + 32 * a) * LD + c0 + jj];
+  double dmin = DBL_MAX;
+#pragma unroll
+  for (int jj = 0; jj < 8; ++jj) {
+    const int k = c0 + jj;
+    if (k >= Q) break;
+    const int lk = k & 31;
+    uint64_t key[RW];
+    uint64_t best = 0;
+#pragma unroll
+    for (int a = AK; a < RW; ++a) {
+      const int i = lane + 32 * a;
+      key[a] = (i >= k && i < Q) ? (uint64_t)__double_as_longlong(fabs(P[jj][a])) + 1ull : 0ull;
+      best = key[a] > best ? key[a] : best;
+    }
+    const unsigned hi = (unsigned)(best >> 32);
+    const unsigned mhi = __reduce_max_sync(kFull, hi);
+    const unsigned lo = hi == mhi ? (unsigned)(best & 0xffffffffu) : 0u;
+    const unsigned mlo = __reduce_max_sync(kFull, lo);
+    const uint64_t mk = ((uint64_t)mhi << 32) | mlo;
+    int p = k;
+#pragma unroll
+    for (int a = RW - 1; a >= AK; --a) {
+      const unsigned m = __ballot_sync(kFull, key[a] == mk);
+      if (m) p = 32 * a + __ffs(m) - 1;
+    }
+    const int ap = p >> 5, lp = p & 31;
+    double pv;
+    if (p == k) {
+      pv = __shfl_sync(kFull, P[jj][AK], lk);
+    } else {
+      pv = __shfl_sync(kFull, pick_r<RW>(P[jj], ap), lp);
+      if (pv != 0.0) {  // exchange rows k and p inside the panel
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const double vk = __shfl_sync(kFull, P[c][AK], lk);
+          const double vp = __shfl_sync(kFull, pick_r<RW>(P[c], ap), lp);
+#pragma unroll
+          for (int a = AK; a < RW; ++a) {
+            if (a == AK) P[c][a] = osel(lane == lk, vp, P[c][a]);
+            P[c][a] = osel(a == ap && lane == lp, vk, P[c][a]);
+          }
+        }
+      }
+    }
+    const double rcp = __drcp_rn(pv);
+    const bool scale = pv != 0.0, big = fabs(pv) >= DBL_MIN;
+#pragma unroll
+    for (int a = AK; a < RW; ++a) {
+      const int i = lane + 32 * a;
+      if (i > k && i < Q && scale) P[jj][a] = big ? P[jj][a] * rcp : P[jj][a] / pv;
+    }
+#pragma unroll
+    for (int c = jj + 1; c < 8; ++c) {  // rank-1 update inside the panel
+      const double u = __shfl_sync(kFull, P[c][AK], lk);
+#pragma unroll
+      for (int a = AK; a < RW; ++a)
+        if (lane + 32 * a > k) P[c][a] = fma(-P[jj][a], u, P[c][a]);
+    }
+    if (lane == 0) {
+      const int pe = scale ? p : k;
+      s_pv[jj] = pe;
+      piv[k] = p;
+      if (pe != k) {
+        const int tmp = s_perm[k];
+        s_perm[k] = s_perm[pe];
+        s_perm[pe] = tmp;
+      }
+    }
+    dmin = fmin(dmin, fabs(pv));
+  }
+#pragma unroll
+  for (int jj = 0; jj < 8; ++jj)
+#pragma unroll
+    for (int a = AK; a < RW; ++a) {
+      const int i = lane + 32 * a;
+      if (i >= c0) Ws[i * LD + c0 + jj] = P[jj][a];
+    }
+  return dmin;
+}
+
+template <int RW, int LD>
+__device__ __forceinline__ double panel_dispatch(double* Ws, int c0, int Q, int lane, int* s_pv,
+                                                 int* s_perm, int* piv) {
+  switch (c0 >> 5) {
+    case 0: return panel_factor<RW, LD, 0>(Ws, c0, Q, lane, s_pv, s_perm, piv);
+    case 1: if (RW > 1) return panel_factor<RW, LD, (RW > 1 ? 1 : 0)>(Ws, c0, Q, lane, s_pv, s_perm, piv); break;
+    case 2: if (RW > 2) return panel_factor<RW, LD, (RW > 2 ? 2 : 0)>(Ws, c0, Q, lane, s_pv, s_perm, piv); break;
+    case 3: if (RW > 3) return panel_factor<RW, LD, (RW > 3 ? 3 : 0)>(Ws, c0, Q, lane, s_pv, s_perm, piv); break;
+  }
+  return DBL_MAX;
+}
+
 template <int RW, int LD>
 __global__ void __launch_bounds__(256) lu_dmma_kernel(LuArgs g) {
-  constexpr int QP = 32 * RW;
+  constexpr int QP = 32 * RW, NTQ = QP / 8;
   constexpr int NT = 256, NW = 8;
   extern __shared__ double Ws[];  // QP x LD row-major
   __shared__ int s_pv[8];
@@ -411,6 +531,7 @@ __global__ void __launch_bounds__(256) lu_dmma_kernel(LuArgs g) {
   const int64_t e = blockIdx.x;
   const int Q = g.Q;
   const double* __restrict__ Ae = g.A + e * (int64_t)Q * Q;
+  int* piv = g.piv + e * Q;
 
   double amax = 0.0;
   for (int idx = tid; idx < QP * QP; idx += NT) {
@@ -428,92 +549,11 @@ __global__ void __launch_bounds__(256) lu_dmma_kernel(LuArgs g) {
   for (int i = 0; i < NW; ++i) amax = fmax(amax, red[i]);
   double dmin = DBL_MAX;
   const int npanel = (Q + 7) / 8;
+  if (warp == 0) dmin = panel_dispatch<RW, LD>(Ws, 0, Q, lane, s_pv, s_perm, piv);
+  __syncthreads();
 
   for (int pnl = 0; pnl < npanel; ++pnl) {
     const int c0 = pnl * 8;
-    // ---- 1. panel factorisation (warp 0, rows c0.., columns c0..c0+7)
-    if (warp == 0) {
-      double P[8][RW];
-#pragma unroll
-      for (int jj = 0; jj < 8; ++jj)
-#pragma unroll
-        for (int a = 0; a < RW; ++a) {
-          const int i = lane + 32 * a;
-          P[jj][a] = (i >= c0) ? Ws[i * LD + c0 + jj] : 0.0;
-        }
-#pragma unroll
-      for (int jj = 0; jj < 8; ++jj) {
-        const int k = c0 + jj;
-        if (k >= Q) break;
-        // idamax over rows k..Q-1 of panel column jj
-        uint64_t key[RW];
-        uint64_t best = 0;
-#pragma unroll
-        for (int a = 0; a < RW; ++a) {
-          const int i = lane + 32 * a;
-          key[a] = (i >= k && i < Q) ? (uint64_t)__double_as_longlong(fabs(P[jj][a])) + 1ull : 0ull;
-          best = key[a] > best ? key[a] : best;
-        }
-        const unsigned hi = (unsigned)(best >> 32);
-        const unsigned mhi = __reduce_max_sync(kFull, hi);
-        const unsigned lo = hi == mhi ? (unsigned)(best & 0xffffffffu) : 0u;
-        const unsigned mlo = __reduce_max_sync(kFull, lo);
-        const uint64_t mk = ((uint64_t)mhi << 32) | mlo;
-        int p = k;
-#pragma unroll
-        for (int a = RW - 1; a >= 0; --a) {
-          const unsigned m = __ballot_sync(kFull, key[a] == mk);
-          if (m) p = 32 * a + __ffs(m) - 1;
-        }
-        const int ak = k >> 5, lk = k & 31, ap = p >> 5, lp = p & 31;
-        const double pv = __shfl_sync(kFull, pick_r<RW>(P[jj], ap), lp);
-        if (p != k && pv != 0.0) {  // exchange rows k and p inside the panel
-#pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const double vk = __shfl_sync(kFull, pick_r<RW>(P[c], ak), lk);
-            const double vp = __shfl_sync(kFull, pick_r<RW>(P[c], ap), lp);
-#pragma unroll
-            for (int a = 0; a < RW; ++a) {
-              P[c][a] = osel(a == ak && lane == lk, vp, P[c][a]);
-              P[c][a] = osel(a == ap && lane == lp, vk, P[c][a]);
-            }
-          }
-        }
-        const bool big = fabs(pv) >= DBL_MIN;
-        const double rcp = 1.0 / pv;
-#pragma unroll
-        for (int a = 0; a < RW; ++a) {
-          const int i = lane + 32 * a;
-          if (i > k && i < Q && pv != 0.0) P[jj][a] = big ? P[jj][a] * rcp : P[jj][a] / pv;
-        }
-#pragma unroll
-        for (int c = jj + 1; c < 8; ++c) {  // rank-1 update inside the panel
-          const double u = __shfl_sync(kFull, pick_r<RW>(P[c], ak), lk);
-#pragma unroll
-          for (int a = 0; a < RW; ++a)
-            if (lane + 32 * a > k) P[c][a] = fma(-P[jj][a], u, P[c][a]);
-        }
-        if (lane == 0) {
-          const int pe = (pv != 0.0) ? p : k;
-          s_pv[jj] = pe;
-          g.piv[e * Q + k] = p;
-          if (pe != k) {
-            const int tmp = s_perm[k];
-            s_perm[k] = s_perm[pe];
-            s_perm[pe] = tmp;
-          }
-          dmin = fmin(dmin, fabs(pv));
-        }
-      }
-#pragma unroll
-      for (int jj = 0; jj < 8; ++jj)
-#pragma unroll
-        for (int a = 0; a < RW; ++a) {
-          const int i = lane + 32 * a;
-          if (i >= c0) Ws[i * LD + c0 + jj] = P[jj][a];
-        }
-    }
-    __syncthreads();
     // ---- 2. row exchanges outside the panel + U12 = L11^-1 A12
     const int ncolp = min(8, Q - c0);
     for (int j = tid; j < QP; j += NT) {
@@ -539,22 +579,25 @@ __global__ void __launch_bounds__(256) lu_dmma_kernel(LuArgs g) {
       }
     }
     __syncthreads();
-    // ---- 3. A22 -= L21 U12 on 8x8 tiles with DMMA
-    const int t0 = pnl + 1, nt = QP / 8 - t0;
-    if (nt > 0) {
-      const int r = lane >> 2, q = lane & 3;
-      for (int tile = warp; tile < nt * nt; tile += NW) {
-        const int ti = t0 + tile / nt, tj = t0 + tile % nt;
-        const int row = ti * 8 + r, col = tj * 8 + 2 * q;
-        double d0 = Ws[row * LD + col], d1 = Ws[row * LD + col + 1];
-#pragma unroll
-        for (int k0 = 0; k0 < 8; k0 += 4) {
-          const double av = -Ws[row * LD + c0 + k0 + q];           // A: row r, k = q
-          const double bv = Ws[(c0 + k0 + q) * LD + tj * 8 + r];   // B: k = q, col r
-          dmma_8x8x4(d0, d1, av, bv);
+    // ---- 3. trailing update; warp 0 runs ahead to the next panel
+    const int t0 = pnl + 1;
+    if (t0 < NTQ) {
+      if (warp == 0) {
+        for (int ti = t0; ti < NTQ; ++ti) tile_update<LD>(Ws, c0, ti, t0, lane);
+        __syncwarp();
+        if (pnl + 1 < npanel)
+          dmin = fmin(dmin, panel_dispatch<RW, LD>(Ws, c0 + 8, Q, lane, s_pv, s_perm, piv));
+      } else {
+        const int ncol = NTQ - t0 - 1;  // tile columns t0+1 .. NTQ-1
+        if (ncol > 0) {
+          int ti = t0, tj = t0 + 1 + (warp - 1);
+          while (tj >= NTQ) { tj -= ncol; ++ti; }
+          while (ti < NTQ) {
+            tile_update<LD>(Ws, c0, ti, tj, lane);
+            tj += NW - 1;
+            while (tj >= NTQ) { tj -= ncol; ++ti; }
+          }
         }
-        Ws[row * LD + col] = d0;
-        Ws[row * LD + col + 1] = d1;
       }
     }
     __syncthreads();
