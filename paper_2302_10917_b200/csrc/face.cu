@@ -95,6 +95,51 @@ __global__ void __launch_bounds__(kFaceWarps * 32) face_reduce_kernel(FaceArgs a
   }
 }
 
+// Small faces (t <= G): a group of G lanes (G = 16: two faces per warp) per
+// face, lane g owning row g; every column load of the GEMVs is issued up
+// front (static unroll over TMAX = G columns) for memory-level parallelism.
+template <int G, bool RHS, bool PRE>
+__global__ void __launch_bounds__(kFaceWarps * 32) face_small_kernel(FaceArgs a) {
+  __shared__ double s_u[kFaceWarps * 32];
+  constexpr int FPB = kFaceWarps * 32 / G;  // faces per CTA
+  const int tid = threadIdx.x, g = tid % G, grp = tid / G;
+  const int64_t f = (int64_t)blockIdx.x * FPB + grp;
+  const bool valid_face = f < a.F;
+  const int t = a.t;
+  const size_t TT = (size_t)t * t;
+  const bool row = valid_face && g < t;
+  double* su = s_u + grp * G;
+  double z = row ? __ldg((RHS ? a.Rhat : a.uhat) + f * t + g) : 0.0;
+  const unsigned mask = G == 32 ? kFull : (0xffffu << (tid & 16));
+  if (!RHS) {
+    su[g] = z;
+    __syncwarp(mask);
+    const double* Df = a.D + (valid_face ? f : 0) * TT;
+    double acc = 0.0;
+#pragma unroll
+    for (int s = 0; s < G; ++s)
+      if (s < t && row) acc = fma(__ldg(Df + (size_t)s * t + g), su[s], acc);
+    z = acc;
+    __syncwarp(mask);
+  }
+  if (row) {
+    const int sl = __ldg(a.vslot + 2 * f), sr = __ldg(a.vslot + 2 * f + 1);
+    if (sl >= 0) z -= __ldg(a.V + (int64_t)sl * t + g);  // left first
+    if (sr >= 0) z -= __ldg(a.V + (int64_t)sr * t + g);  // then right
+  }
+  if (PRE) {
+    su[g] = z;
+    __syncwarp(mask);
+    const double* Mi = a.Dinv + (valid_face ? f : 0) * TT;
+    double acc = 0.0;
+#pragma unroll
+    for (int s = 0; s < G; ++s)
+      if (s < t && row) acc = fma(__ldg(Mi + (size_t)s * t + g), su[s], acc);
+    z = acc;
+  }
+  if (row) a.out[f * t + g] = z;
+}
+
 template <int RT>
 __global__ void __launch_bounds__(kFaceWarps * 32) precond_kernel(FaceArgs a) {
   extern __shared__ double s_buf[];
@@ -352,9 +397,26 @@ int launch_face_factor(mh_system* s, const double* Drm) {
   return MH_OK;
 }
 
+template <int G>
+int launch_small(mh_system* s, const FaceArgs& a, int rhs_mode, int pre) {
+  constexpr int FPB = kFaceWarps * 32 / G;
+  const unsigned grid = (unsigned)((s->F + FPB - 1) / FPB);
+  if (rhs_mode) {
+    if (pre) face_small_kernel<G, true, true><<<grid, kFaceWarps * 32, 0, s->stream>>>(a);
+    else face_small_kernel<G, true, false><<<grid, kFaceWarps * 32, 0, s->stream>>>(a);
+  } else {
+    if (pre) face_small_kernel<G, false, true><<<grid, kFaceWarps * 32, 0, s->stream>>>(a);
+    else face_small_kernel<G, false, false><<<grid, kFaceWarps * 32, 0, s->stream>>>(a);
+  }
+  MH_CHECK_CUDA(cudaGetLastError());
+  return MH_OK;
+}
+
 int launch_face_reduce(mh_system* s, const double* uhat, double* w, int rhs_mode, int pre) {
   if (s->F == 0) return MH_OK;
   FaceArgs a = make_args(s, uhat, w);
+  if (s->t <= 16) return launch_small<16>(s, a, rhs_mode, pre);
+  if (s->t <= 32) return launch_small<32>(s, a, rhs_mode, pre);
   const unsigned grid = (unsigned)((s->F + kFaceWarps - 1) / kFaceWarps);
   const size_t smem = (size_t)kFaceWarps * s->t * sizeof(double);
   const int RT = (s->t + 31) / 32;
