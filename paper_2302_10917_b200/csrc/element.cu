@@ -172,6 +172,7 @@ element_kernel(ElemArgs a) {
   uint64_t* empty = full + kWPB * S;
   double* su_all = reinterpret_cast<double*>(empty + kWPB * S);
   const int nseg = (MODE != kRhs ? 1 : 0) + 2 + (MODE != kRecon ? 1 : 0);
+  (void)t;
   if (threadIdx.x == 0) {
     int n = 0;
     if (MODE != kRhs) segs[n++] = Segment{a.Bt, a.ldB, nchB, (MODE == kApply && a.c_is_bt) ? 1 : 0};
@@ -198,32 +199,72 @@ element_kernel(ElemArgs a) {
   const uint32_t offC = offU + (uint32_t)a.ldL;
   const uint32_t E = offC + ((MODE != kRecon) ? (uint32_t)a.ldB : 0u);
 
+  // Software pipeline over a warp's macros: the small per-macro vectors of
+  // the NEXT macro (perm, 1/U_jj, face table, gathered uhat) are loaded while
+  // this one is processed, so their latency never sits at the start of a macro.
+  constexpr int RC = 8;  // gathered slot values per lane (nc <= 256)
+  int pr_n[R];
+  double dr_n[R];
+  int32_t ef_n[4];
+  double g_n[RC];
+  auto load_meta = [&](int64_t en) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = lane + 32 * r;
+      pr_n[r] = i < Q ? __ldg(a.perm + en * Q + i) : i;
+      dr_n[r] = i < Q ? __ldg(a.dinv + en * Q + i) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) ef_n[k] = k < a.nfe ? __ldg(a.elem_ufac + en * a.nfe + k) : -1;
+  };
+  auto gather_next = [&]() {
+#pragma unroll
+    for (int q = 0; q < RC; ++q) {
+      const int c = lane + 32 * q;
+      double v = 0.0;
+      if (c < nc) {
+        const int k = c / t, s = c - k * t;
+        int f = ef_n[0];
+#pragma unroll
+        for (int kk = 1; kk < 4; ++kk) f = (k == kk) ? ef_n[kk] : f;
+        if (f >= 0)
+          v = f < a.F ? __ldg(a.uhat + (int64_t)f * t + s)
+                      : __ldg(a.uhalo + (int64_t)(f - a.F) * t + s);
+      }
+      g_n[q] = v;
+    }
+  };
+  const int64_t e_first = (int64_t)blockIdx.x * kWPB + w;
+  if (e_first < a.N) {
+    load_meta(e_first);
+    if (MODE != kRhs) gather_next();
+  }
+
   uint32_t base = 0;
-  for (int64_t e = (int64_t)blockIdx.x * kWPB + w; e < a.N; e += W, base += E) {
+  for (int64_t e = e_first; e < a.N; e += W, base += E) {
     int pr[R];
     double dr[R];
     bool ident = true;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int i = lane + 32 * r;
-      pr[r] = i < Q ? __ldg(a.perm + e * Q + i) : i;
-      dr[r] = i < Q ? __ldg(a.dinv + e * Q + i) : 0.0;
+      pr[r] = pr_n[r];
+      dr[r] = dr_n[r];
       ident = ident && pr[r] == i;
     }
+    if (MODE != kRhs) {
+#pragma unroll
+      for (int q = 0; q < RC; ++q)
+        if (lane + 32 * q < nc) su[lane + 32 * q] = g_n[q];
+    }
+    const int64_t en = e + W;
+    if (en < a.N) load_meta(en);  // lands while this macro is processed
     const bool has_perm = !__all_sync(kFull, ident);
     double y[R];
     if (MODE == kRhs) {
 #pragma unroll
       for (int r = 0; r < R; ++r) y[r] = (lane + 32 * r < Q) ? __ldg(a.Ru + e * Q + pr[r]) : 0.0;
     } else {
-      const int32_t* ef = a.elem_ufac + e * a.nfe;
-      for (int c = lane; c < nc; c += 32) {
-        const int k = c / t, s = c - k * t;
-        const int f = __ldg(ef + k);
-        su[c] = f < 0 ? 0.0
-                : (f < a.F ? __ldg(a.uhat + (int64_t)f * t + s)
-                           : __ldg(a.uhalo + (int64_t)(f - a.F) * t + s));
-      }
       __syncwarp();
       double acc[R];
 #pragma unroll
@@ -242,7 +283,8 @@ element_kernel(ElemArgs a) {
         cs.window(p, p + Q, lane);
         gemv_rows<R, 1, RING, true, true>(acc, ring, p, Q, su + c, pr, lane);
       }
-      __syncwarp();  // su is rewritten by the next macro
+      __syncwarp();  // su is rewritten for the next macro
+      if (en < a.N) gather_next();  // its face table arrived during step 1
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         if (MODE == kApply) y[r] = acc[r];
