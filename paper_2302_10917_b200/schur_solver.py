@@ -324,15 +324,28 @@ def condense_arrays(mesh, A, B, Cm, R_u, D, R_hat, config: SolverConfig, *, p: i
 
 
 def condense(mesh, local_ops: list, face_ops: dict, config: SolverConfig,
-             pool: Optional[WorkerPool] = None) -> CondensedSystem:
+             pool: Optional[WorkerPool] = None, host_factors: bool = False) -> CondensedSystem:
     """schur_solver.py:185-254: factorise every block on the device and form
-    f = R_hat - sum C A^-1 R_u."""
+    f = R_hat - sum C A^-1 R_u.
+
+    The reference stores scipy factors in ``op.lu`` / ``op.factor`` (mutating
+    its inputs, schur_solver.py:111, 137-147).  Here the factors stay on the
+    device; ``host_factors=True`` copies them back into those fields in the
+    reference's layout (``("dense", (lu, piv))``; faces ``("inv", 1.0, D^-1)``)."""
     tables = mesh_tables(mesh)
     tables.update(condense_tables(tables))
     A, B, Cm, Ru, D, Rh, nloc, t = _stack_ops(local_ops, face_ops, tables)
     m = mesh.macro_elements[0].m if len(mesh.macro_elements) else 1
-    return condense_arrays(mesh, A, B, Cm, Ru, D, Rh, config, p=_infer_p(nloc, m),
-                           tables=tables, local_ops=local_ops, face_ops=face_ops, pool=pool)
+    sys = condense_arrays(mesh, A, B, Cm, Ru, D, Rh, config, p=_infer_p(nloc, m),
+                          tables=tables, local_ops=local_ops, face_ops=face_ops, pool=pool)
+    if host_factors:
+        lu, piv = local_factors(sys)
+        for e, op in enumerate(local_ops):
+            op.lu = ("dense", (lu[e], piv[e]))
+        for u, fid in enumerate(sys.face_ids):
+            fop = face_ops[int(fid)]
+            fop.factor = ("inv", 1.0, np.linalg.inv(fop.D))
+    return sys
 
 
 def _infer_p(nloc: int, m: int) -> int:

@@ -307,3 +307,46 @@ def test_element_schur_blocks_match_oracle(gpu):
     for e in range(prob["N"]):
         ref = -(o.C[e] @ sla.lu_solve(o.lu[e], o.B[e]))
         assert np.abs(blocks[e] - ref).max() <= APPLY_TOL * np.abs(ref).max()
+
+
+def test_preconditioner_round_trip(c1):
+    """test_schur_solver.py:127-135: D^-1 (D x) = x to 1e-12."""
+    prob, sys_, _ = c1
+    x = np.random.default_rng(1).standard_normal(sys_.zhat)
+    t = prob["t"]
+    w = np.concatenate([prob["D"][u] @ x[u * t:(u + 1) * t] for u in range(prob["F"])])
+    back = P.apply_preconditioner(sys_, w)
+    assert np.abs(back - x).max() < 1e-12 * max(1.0, np.abs(x).max())
+
+
+def test_host_factors_and_solve_driver(gpu):
+    """condense(host_factors=True) fills op.lu like the reference; solve() with an
+    assemble callable runs condense -> GMRES -> reconstruct and reports."""
+    g = golden("real_tanh_n2m2p2.npz")
+    n, m, p = int(g["n"]), int(g["m"]), int(g["p"])
+    mesh = P.build_structured_macro_mesh(2, n, m)
+    t = g["D"].shape[1]
+
+    def assemble(mesh_, problem, stab, p_):
+        local_ops = [P.LocalOperators(macro_id=e, A=g["A"][e], B=g["B"][e], C=g["C"][e],
+                                      R_u=g["R_u"][e],
+                                      face_slots=[(int(f), slice(k * t, (k + 1) * t))
+                                                  for k, f in enumerate(g["slot_faces"][e])])
+                     for e in range(g["A"].shape[0])]
+        face_ops = {int(f): P.FaceOperator(face_id=int(f), D=g["D"][i], R_hat=g["R_hat"][i])
+                    for i, f in enumerate(g["face_ids"])}
+        return local_ops, face_ops
+
+    lops, fops = assemble(mesh, None, None, p)
+    sys_ = P.condense(mesh, lops, fops, P.SolverConfig(tol=1e-12), host_factors=True)
+    for e, op in enumerate(lops):
+        assert op.lu[0] == "dense"
+        assert np.array_equal(op.lu[1][1], g["piv"][e])
+        assert np.abs(op.lu[1][0] - g["lu"][e]).max() <= 1e-12 * np.abs(g["lu"][e]).max()
+    sol, sys2 = P.solve(mesh, None, None, P.SolverConfig(tol=1e-12), p, assemble=assemble)
+    rec = sol.report.to_record()
+    assert rec["converged"] and abs(rec["iterations"] - int(g["iterations"])) <= 1
+    assert rel(sol.uhat, g["x"]) <= SOLVE_TOL
+    assert rel(np.stack(sol.local), g["U"]) <= SOLVE_TOL
+    with pytest.raises(NotImplementedError):
+        P.solve(mesh, None, None, P.SolverConfig(), p)
