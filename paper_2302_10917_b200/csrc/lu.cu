@@ -20,6 +20,8 @@
 
 #include <algorithm>
 #include <cfloat>
+#include <cstdlib>
+#include <string>
 
 #include "mh_internal.h"
 
@@ -51,6 +53,7 @@ struct LuArgs {
   int32_t* perm;     // N x Q
   int32_t* stat;     // N
   int64_t ldL;
+  int64_t nblocks;
   int Q;
   int use_smem;
 };
@@ -626,6 +629,223 @@ __global__ void __launch_bounds__(256) lu_dmma_kernel(LuArgs g) {
   if (tid == 0) g.stat[e] = (dmin <= 1e-13 * fmax(amax, 1e-300)) ? 1 : 0;
 }
 
+// ---------------------------------------------------------------------------
+// Left-looking blocked variant: ONE WARP PER BLOCK, no shared-memory copy of
+// the matrix, so many blocks are in flight per SM (the limiter of the
+// CTA-per-block kernels is the dependent pivot chain of each block).
+//
+// Rows are tracked by position (prow[i] = original row now at position i, the
+// composed LAPACK permutation).  For each 8-column panel (columns c0..c0+7):
+//   1. gather the panel rows of the ORIGINAL matrix through prow (each entry
+//      of A is read exactly once overall);
+//   2. for every previous panel kb: U_kb = L11(kb)^-1 rows(kb) (8x8 solve,
+//      lanes over columns, via a per-warp shared 8x8 tile), written to the
+//      packed U stream, then rows below -= L(rows, kb) U_kb (L read back from
+//      the packed L stream -- L2 resident);
+//   3. factor the panel (idamax via REDUX, LAPACK row exchange -- mirrored on
+//      the already stored L rows, rare --, reciprocal scaling, rank-1 updates);
+//   4. store L (packed, by position), U (packed) and the diagonal.
+// The factors land directly in the streams the element kernel reads.
+template <int R>
+__device__ __forceinline__ double lpk(const double* Lpe, int i, int j, int Q) {
+  return Lpe[off_lower(j, Q) + (i - j - 1)];
+}
+
+constexpr int kLeftWarps = 4;  // blocks (one per warp) per CTA
+
+template <int R>
+__global__ void __launch_bounds__(kLeftWarps * 32) lu_left_kernel(LuArgs g) {
+  __shared__ double Ssh[kLeftWarps][64];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t e = (int64_t)blockIdx.x * kLeftWarps + w;
+  const int Q = g.Q;
+  if (e >= g.nblocks) return;
+  const double* __restrict__ Ae = g.A + e * (int64_t)Q * Q;
+  double* Lpe = g.Lp + e * g.ldL;  // L is stored in place (L2 resident while in use)
+  double* Upe = g.Up + e * g.ldL;
+  int* piv = g.piv + e * Q;
+  double* S = Ssh[w];
+
+  int prow[R];
+#pragma unroll
+  for (int a = 0; a < R; ++a) prow[a] = lane + 32 * a;
+  double amax = 0.0, dmin = DBL_MAX;
+  const int npanel = (Q + 7) / 8;
+
+  for (int jb = 0; jb < npanel; ++jb) {
+    const int c0 = 8 * jb;
+    const int ncol = min(8, Q - c0);
+    // ---- 1. gather the panel (rows by position)
+    double P[8][R];
+#pragma unroll
+    for (int a = 0; a < R; ++a) {
+      const int i = lane + 32 * a;
+      const double* row = Ae + (int64_t)prow[a] * Q + c0;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const double v = (i < Q && c < ncol) ? __ldg(row + c) : 0.0;
+        P[c][a] = v;
+        amax = fmax(amax, fabs(v));
+      }
+    }
+    // ---- 2. left-looking update with the previous panels
+    for (int kb = 0; kb < jb; ++kb) {
+      const int k0 = 8 * kb;
+      // (a) rows k0..k0+7 of the panel -> S (8 x 8, row-major)
+#pragma unroll
+      for (int a = 0; a < R; ++a) {
+        const int i = lane + 32 * a;
+        if (i >= k0 && i < k0 + 8)
+#pragma unroll
+          for (int c = 0; c < 8; ++c) S[(i - k0) * 8 + c] = P[c][a];
+      }
+      __syncwarp();
+      if (lane < 8) {  // unit-lower solve, lane = panel column
+        double u[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) u[r] = S[r * 8 + lane];
+#pragma unroll
+        for (int r = 1; r < 8; ++r)
+#pragma unroll
+          for (int m = 0; m < r; ++m) u[r] = fma(-lpk<R>(Lpe, k0 + r, k0 + m, Q), u[m], u[r]);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          S[r * 8 + lane] = u[r];
+          if (lane < ncol) Upe[off_upper(c0 + lane, Q) + k0 + r] = u[r];
+        }
+      }
+      __syncwarp();
+      // (b) rows below: P -= L(rows, k0..k0+7) U_kb
+#pragma unroll
+      for (int a = 0; a < R; ++a) {
+        const int i = lane + 32 * a;
+        if (i >= k0 + 8 && i < Q) {
+          double l[8];
+#pragma unroll
+          for (int m = 0; m < 8; ++m) l[m] = lpk<R>(Lpe, i, k0 + m, Q);
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            double acc = P[c][a];
+#pragma unroll
+            for (int m = 0; m < 8; ++m) acc = fma(-l[m], S[m * 8 + c], acc);
+            P[c][a] = acc;
+          }
+        }
+      }
+      __syncwarp();
+    }
+    // ---- 3. factor the panel (positions >= c0)
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      const int k = c0 + jj;
+      if (jj >= ncol) break;
+      const int lk = k & 31, ak = k >> 5;
+      uint64_t key[R];
+      uint64_t best = 0;
+#pragma unroll
+      for (int a = 0; a < R; ++a) {
+        const int i = lane + 32 * a;
+        key[a] = (i >= k && i < Q) ? (uint64_t)__double_as_longlong(fabs(P[jj][a])) + 1ull : 0ull;
+        best = key[a] > best ? key[a] : best;
+      }
+      const unsigned hi = (unsigned)(best >> 32);
+      const unsigned mhi = __reduce_max_sync(kFull, hi);
+      const unsigned lo = hi == mhi ? (unsigned)(best & 0xffffffffu) : 0u;
+      const unsigned mlo = __reduce_max_sync(kFull, lo);
+      const uint64_t mk = ((uint64_t)mhi << 32) | mlo;
+      int p = k;
+#pragma unroll
+      for (int a = R - 1; a >= 0; --a) {
+        const unsigned m = __ballot_sync(kFull, key[a] == mk);
+        if (m) p = 32 * a + __ffs(m) - 1;
+      }
+      const int ap = p >> 5, lp = p & 31;
+      const double pv = __shfl_sync(kFull, pick_r<R>(P[jj], ap), lp);
+      if (p != k && pv != 0.0) {
+        // exchange positions k and p: panel values, prow, stored L rows
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const double vk = __shfl_sync(kFull, pick_r<R>(P[c], ak), lk);
+          const double vp = __shfl_sync(kFull, pick_r<R>(P[c], ap), lp);
+#pragma unroll
+          for (int a = 0; a < R; ++a) {
+            P[c][a] = osel(a == ak && lane == lk, vp, P[c][a]);
+            P[c][a] = osel(a == ap && lane == lp, vk, P[c][a]);
+          }
+        }
+        int rk = 0, rp = 0;
+#pragma unroll
+        for (int a = 0; a < R; ++a) {
+          const int xk = __shfl_sync(kFull, prow[a], lk);
+          const int xp = __shfl_sync(kFull, prow[a], lp);
+          if (a == ak) rk = xk;
+          if (a == ap) rp = xp;
+        }
+#pragma unroll
+        for (int a = 0; a < R; ++a) {
+          if (a == ak && lane == lk) prow[a] = rp;
+          if (a == ap && lane == lp) prow[a] = rk;
+        }
+        for (int j = lane; j < c0; j += 32) {  // stored L rows k, p (columns < c0)
+          double* ck = Lpe + off_lower(j, Q) + (k - j - 1);
+          double* cp = Lpe + off_lower(j, Q) + (p - j - 1);
+          const double t = *ck;
+          *ck = *cp;
+          *cp = t;
+        }
+        __syncwarp();
+      }
+      const bool scale = pv != 0.0, big = fabs(pv) >= DBL_MIN;
+      const double rcp = __drcp_rn(pv);
+#pragma unroll
+      for (int a = 0; a < R; ++a) {
+        const int i = lane + 32 * a;
+        if (i > k && i < Q && scale) P[jj][a] = big ? P[jj][a] * rcp : P[jj][a] / pv;
+      }
+#pragma unroll
+      for (int c = jj + 1; c < 8; ++c) {
+        const double u = __shfl_sync(kFull, pick_r<R>(P[c], ak), lk);
+#pragma unroll
+        for (int a = 0; a < R; ++a)
+          if (lane + 32 * a > k) P[c][a] = fma(-P[jj][a], u, P[c][a]);
+      }
+      if (lane == 0) piv[k] = p;
+      dmin = fmin(dmin, fabs(pv));
+    }
+    // ---- 4. store: L below the diagonal, U above (within the panel), diag
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      if (c >= ncol) break;
+      const int j = c0 + c;
+      const int64_t ol = off_lower(j, Q), ou = off_upper(j, Q);
+#pragma unroll
+      for (int a = 0; a < R; ++a) {
+        const int i = lane + 32 * a;
+        if (i >= Q || i < c0) continue;
+        const double v = P[c][a];
+        if (i > j) Lpe[ol + (i - j - 1)] = v;
+        else if (i < j) Upe[ou + i] = v;
+        else {
+          g.udiag[e * Q + i] = v;
+          g.dinv[e * Q + i] = 1.0 / v;
+        }
+      }
+    }
+    __syncwarp();
+  }
+  for (int64_t i = (int64_t)Q * (Q - 1) / 2 + lane; i < g.ldL; i += 32) {
+    Lpe[i] = 0.0;
+    Upe[i] = 0.0;
+  }
+#pragma unroll
+  for (int a = 0; a < R; ++a) {
+    const int i = lane + 32 * a;
+    if (i < Q) g.perm[e * Q + i] = prow[a];
+  }
+  for (int o = 16; o; o >>= 1) amax = fmax(amax, __shfl_xor_sync(kFull, amax, o));
+  if (lane == 0) g.stat[e] = (dmin <= 1e-13 * fmax(amax, 1e-300)) ? 1 : 0;
+}
+
 __global__ void unpack_lu_kernel(const double* __restrict__ Lp, const double* __restrict__ Up,
                                  const double* __restrict__ udiag, int64_t ldL, int Q,
                                  int64_t first, int64_t count, double* __restrict__ out) {
@@ -688,24 +908,44 @@ int launch_lu(mh_system* s, float* ms) {
   g.perm = s->perm.p;
   g.stat = s->lstat.p;
   g.ldL = s->ldL;
+  g.nblocks = s->N;
   g.Q = s->Q;
   g.use_smem = use_smem;
   const int Q = s->Q;
   const unsigned grid = (unsigned)s->N;
-  if (Q <= 32) lu_reg_kernel<1, 4, 8><<<grid, 256, 0, s->stream>>>(g);
-  else if (Q <= 64) {
+  // kernel choice: warp-per-block left-looking for Q > 32 (fastest measured at
+  // c2/c3 and the only one without a shared-memory size limit); MEHDG_LU=dmma|reg
+  // selects the CTA-per-block kernels for comparison
+  const char* var = getenv("MEHDG_LU");
+  const std::string choice = var ? std::string(var) : std::string();
+  const bool left = choice == "left" || (choice.empty() && Q > 32) ||
+                    (choice == "dmma" && Q > 96) || (choice == "reg" && Q > 128);
+  if (left) {
+    const unsigned gw = (unsigned)((s->N + kLeftWarps - 1) / kLeftWarps);
+#define MH_LEFT(RR)                                                   \
+  case RR:                                                            \
+    lu_left_kernel<RR><<<gw, kLeftWarps * 32, 0, s->stream>>>(g);     \
+    break;
+    switch ((Q + 31) / 32) {
+      MH_LEFT(1) MH_LEFT(2) MH_LEFT(3) MH_LEFT(4) MH_LEFT(5) MH_LEFT(6) MH_LEFT(7)
+      default: MH_LEFT(8)
+    }
+#undef MH_LEFT
+  } else if (Q <= 32) lu_reg_kernel<1, 4, 8><<<grid, 256, 0, s->stream>>>(g);
+  else if (Q <= 64 && choice != "reg") {
     constexpr int LD = 68;
     const size_t sm = (size_t)64 * LD * sizeof(double);
     MH_CHECK_CUDA(cudaFuncSetAttribute(lu_dmma_kernel<2, LD>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     lu_dmma_kernel<2, LD><<<grid, 256, sm, s->stream>>>(g);
-  } else if (Q <= 96) {
+  } else if (Q <= 96 && choice != "reg") {
     constexpr int LD = 100;
     const size_t sm = (size_t)96 * LD * sizeof(double);
     MH_CHECK_CUDA(cudaFuncSetAttribute(lu_dmma_kernel<3, LD>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     lu_dmma_kernel<3, LD><<<grid, 256, sm, s->stream>>>(g);
-  }
+  } else if (Q <= 64) lu_reg_kernel<2, 8, 8><<<grid, 256, 0, s->stream>>>(g);
+  else if (Q <= 96) lu_reg_kernel<3, 12, 8><<<grid, 256, 0, s->stream>>>(g);
   else if (Q <= 128) lu_reg_kernel<4, 8, 16><<<grid, 512, 0, s->stream>>>(g);
   else {
     if (!use_smem) {
