@@ -14,6 +14,7 @@ __version__ = "0.1.0"
 
 _EXPORTS = {
     "assembly": ["FaceOperator", "LocalOperators", "operators_from_problem"],
+    "io": ["export_text", "read_csv", "rows_to_csv", "write_csv"],
     "mesh": ["FaceSide", "MacroElement", "SkeletonFace", "StructuredMacroMesh",
              "build_structured_macro_mesh", "condense_tables", "mesh_tables"],
     "schur_solver": ["CondensedSystem", "Preconditioner", "SchurOperator", "SingularFaceBlock",

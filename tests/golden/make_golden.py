@@ -61,6 +61,7 @@ def make_skeletons():
         M = R_mesh.build_structured_macro_mesh(2, n, 2)
         for k, v in ref_skeleton_tables(M).items():
             out[f"n{n}_{k}"] = v
+        out[f"n{n}_export_text"] = np.frombuffer(R_mesh.export_text(M).encode(), np.uint8)
     np.savez_compressed(HERE / "skeleton_2d.npz", **out)
     out = {}
     for n in (1, 2, 3, 4):

@@ -132,3 +132,27 @@ def test_create_without_gpu_fails_loudly():
     h = C.c_void_p()
     st = _lib.lib.mh_create(0, 3, 2, 15, 5, 1, C.byref(h))
     assert st == _lib.MH_E_CUDA
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 8])
+def test_export_text_matches_reference(n):
+    """mesh.py:479-490 dump of our C++-built mesh equals the reference's, byte for byte."""
+    import paper_2302_10917_b200 as P
+
+    g = golden("skeleton_2d.npz")
+    ref = bytes(g[f"n{n}_export_text"]).decode()
+    assert P.export_text(build_structured_macro_mesh(2, n, 2)) == ref
+
+
+def test_report_csv_round_trip(tmp_path):
+    """17-significant-digit CSV (bench.py:328-379) round-trips report records."""
+    import paper_2302_10917_b200 as P
+
+    rows = [{"p": 3, "m": 4, "n": 128, "tol": 1e-10, "converged": True,
+             "t_init_s": 0.1 + 0.2, "lbf": 1.0, "mode": "mf"}]
+    cols = list(rows[0])
+    path = tmp_path / "r.csv"
+    P.write_csv(rows, cols, str(path))
+    back = P.read_csv(str(path))
+    assert back == rows
+    assert P.rows_to_csv(rows, cols).splitlines()[1].split(",")[5] == "0.30000000000000004"
