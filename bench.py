@@ -388,6 +388,27 @@ def run_ours(args, world, rank, local):
     e2e_wall = time.perf_counter() - t0
     e2e_ms = max_over_ranks(max(e0.elapsed_time(e1), e2e_wall * 1e3) / e2e_steps, world)
 
+    # ---- matrix-based mode (explicit element Schur blocks)
+    mb = None
+    if plan is None and not args.no_mb:
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        P.form_element_schur(sys_)
+        torch.cuda.synchronize(dev)
+        t_form = time.perf_counter() - t0
+        for _ in range(3):
+            check(lib.mh_apply_mb(h, ptr(u), ptr(w)), "apply_mb")
+        mb_steps = max(10, args.steps // 2)
+        e0.record(stream)
+        for _ in range(mb_steps):
+            check(lib.mh_apply_mb(h, ptr(u), ptr(w)), "apply_mb")
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        mb_ms = e0.elapsed_time(e1) / mb_steps
+        mb_bytes = N * (8 * nc * nc + 16 * nc) + F * (8 * t * t + 32 * t)
+        mb = {"applies_per_s": 1e3 / mb_ms, "ms_per_apply": mb_ms, "form_s": t_form,
+              "bytes_per_apply": mb_bytes, "gbs": mb_bytes / (mb_ms * 1e-3) / 1e9}
+
     # ---- full solve (GMRES + D^-1 to 1e-10); the first call allocates the
     # Krylov basis, the second is timed ----------------------------------------
     def run_solve():
@@ -434,6 +455,7 @@ def run_ours(args, world, rank, local):
                   "seconds": t_solve, "ms_per_iteration": t_solve * 1e3 / max(info["iterations"], 1),
                   "first_call_seconds": t_solve_first, "tol": 1e-10},
         "setup_s": {"generate": t_gen, "condense": t_condense},
+        "mb_mode": mb,
         "clocks": sampler.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -460,6 +482,7 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=2048)
     ap.add_argument("--cpu-reps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-mb", action="store_true", help="skip the matrix-based mode timing")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = (1, 0, 0)

@@ -111,12 +111,20 @@ __global__ void __launch_bounds__(kMbWarps * 32) mb_apply_kernel(MbArgs a) {
   }
   __syncwarp();
   const double* Se = a.St + e * (int64_t)nc * nc;
-  for (int cp0 = 0; cp0 < nc; cp0 += 32) {
-    const int cp = cp0 + lane;
-    double acc = 0.0;
-    if (cp < nc)
-      for (int c = 0; c < nc; ++c) acc = fma(__ldg(Se + (size_t)c * nc + cp), su[c], acc);
-    if (cp < nc) a.V[e * nc + cp] = acc;
+  // two 32-slot output groups per pass (nc <= 64 in one pass) for load-level parallelism
+  for (int cp0 = 0; cp0 < nc; cp0 += 64) {
+    const int cpa = cp0 + lane, cpb = cp0 + 32 + lane;
+    const bool va = cpa < nc, vb = cpb < nc;
+    double acca = 0.0, accb = 0.0;
+#pragma unroll 8
+    for (int c = 0; c < nc; ++c) {
+      const double uc = su[c];
+      const double* col = Se + (size_t)c * nc;
+      if (va) acca = fma(__ldg(col + cpa), uc, acca);
+      if (vb) accb = fma(__ldg(col + cpb), uc, accb);
+    }
+    if (va) a.V[e * nc + cpa] = acca;
+    if (vb) a.V[e * nc + cpb] = accb;
   }
 }
 
