@@ -139,7 +139,7 @@ extern "C" int mh_destroy(mh_system* s) {
   cudaSetDevice(s->device);
   if (s->stream) cudaStreamSynchronize(s->stream);
   s->elem_ufac.release(); s->face_vslot.release();
-  s->A.release(); s->LU.release(); s->Lp.release(); s->Up.release(); s->udiag.release();
+  s->A.release(); s->LU.release(); s->lu_scr.release(); s->Lp.release(); s->Up.release(); s->udiag.release();
   s->dinv.release(); s->piv.release(); s->perm.release();
   s->lstat.release(); s->Bt.release(); s->Cm.release(); s->Ru.release(); s->D.release();
   s->Draw.release(); s->Rhat.release(); s->Dinv.release(); s->Fkind.release(); s->V.release();

@@ -23,7 +23,7 @@
 #include <cstdlib>
 #include <string>
 
-#include "mh_internal.h"
+#include "lu_common.cuh"
 
 namespace mh {
 namespace {
@@ -42,29 +42,7 @@ __device__ __forceinline__ double block_max(double v, double* red) {
   return r;
 }
 
-struct LuArgs {
-  const double* A;   // N x Q x Q row-major input
-  double* LU;        // workspace (global variant only)
-  double* Lp;        // N x ldL packed strict lower, columns 0..Q-2
-  double* Up;        // N x ldL packed strict upper, columns Q-1..1
-  double* udiag;     // N x Q
-  double* dinv;      // N x Q
-  int32_t* piv;      // N x Q
-  int32_t* perm;     // N x Q
-  int32_t* stat;     // N
-  int64_t ldL;
-  int64_t nblocks;
-  int Q;
-  int use_smem;
-};
 
-// packed-layout offsets (see element.cu)
-__host__ __device__ __forceinline__ int64_t off_lower(int j, int Q) {
-  return (int64_t)j * (Q - 1) - (int64_t)j * (j - 1) / 2;
-}
-__host__ __device__ __forceinline__ int64_t off_upper(int j, int Q) {
-  return (int64_t)Q * (Q - 1) / 2 - (int64_t)j * (j + 1) / 2;
-}
 
 __global__ void __launch_bounds__(kLuThreads) lu_kernel(LuArgs g) {
   const double* __restrict__ A = g.A;
@@ -182,14 +160,6 @@ __global__ void __launch_bounds__(kLuThreads) lu_kernel(LuArgs g) {
   }
 }
 
-// opaque select: keeps "for a: if (a == x) r[a] = v" from being turned into
-// a dynamically indexed (local-memory) register array access
-__device__ __forceinline__ double osel(bool c, double x, double y) {
-  double r;
-  asm("{\n .reg .pred q;\n setp.ne.b32 q, %3, 0;\n selp.f64 %0, %1, %2, q;\n}"
-      : "=d"(r) : "d"(x), "d"(y), "r"((int)c));
-  return r;
-}
 
 // ---------------------------------------------------------------------------
 // Register-resident variant for Q <= 32 R <= NW NB: the whole block lives in
@@ -389,19 +359,7 @@ __global__ void __launch_bounds__(NW * 32, 512 / (NW * 32)) lu_reg_kernel(LuArgs
 //      warp 0 updates the next panel's tile column first and factors that
 //      panel while warps 1..7 update the rest of the trailing block.
 // Two CTA barriers per 8 columns.
-template <int RW>
-__device__ __forceinline__ double pick_r(const double (&col)[RW], int a_sel) {
-  double v = col[0];
-#pragma unroll
-  for (int a = 1; a < RW; ++a) v = osel(a == a_sel, col[a], v);
-  return v;
-}
 
-__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-               : "+d"(d0), "+d"(d1)
-               : "d"(a), "d"(b));
-}
 
 // one 8x8 tile of A22 -= L21(rows of ti, panel columns) U12(panel rows, cols of tj)
 template <int LD>
@@ -895,7 +853,6 @@ int launch_lu(mh_system* s, float* ms) {
   if (ms) {
     MH_CHECK_CUDA(cudaEventCreate(&e0));
     MH_CHECK_CUDA(cudaEventCreate(&e1));
-    MH_CHECK_CUDA(cudaEventRecord(e0, s->stream));
   }
   LuArgs g;
   g.A = s->A.p;
@@ -913,14 +870,16 @@ int launch_lu(mh_system* s, float* ms) {
   g.use_smem = use_smem;
   const int Q = s->Q;
   const unsigned grid = (unsigned)s->N;
-  // kernel choice: warp-per-block left-looking for Q > 32 (fastest measured at
-  // c2/c3 and the only one without a shared-memory size limit); MEHDG_LU=dmma|reg
-  // selects the CTA-per-block kernels for comparison
+  // kernel choice: warp-per-block tile LU with DMMA updates for Q > 32 (lu_tile.cu);
+  // MEHDG_LU=left|dmma|reg selects the earlier kernels for comparison
   const char* var = getenv("MEHDG_LU");
   const std::string choice = var ? std::string(var) : std::string();
-  const bool left = choice == "left" || (choice.empty() && Q > 32) ||
-                    (choice == "dmma" && Q > 96) || (choice == "reg" && Q > 128);
-  if (left) {
+  const bool tile = (choice.empty() || choice == "tile") && Q > 32;
+  const bool left = choice == "left" || (choice == "dmma" && Q > 96) || (choice == "reg" && Q > 128);
+  if (e0 && !tile) MH_CHECK_CUDA(cudaEventRecord(e0, s->stream));
+  if (tile) {
+    MH_CHECK(launch_lu_tile(s, g, e0));  // records e0 after its scratch allocation
+  } else if (left) {
     const unsigned gw = (unsigned)((s->N + kLeftWarps - 1) / kLeftWarps);
 #define MH_LEFT(RR)                                                   \
   case RR:                                                            \

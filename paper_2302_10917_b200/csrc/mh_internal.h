@@ -94,6 +94,7 @@ struct mh_system {
   // blocks
   mh::DBuf<double> A;      // staged A, N*Q*Q row-major (input of the LU)
   mh::DBuf<double> LU;     // N*Q*Q column-major workspace (only when Q*Q*8 > smem)
+  mh::DBuf<double> lu_scr; // per-warp-slot scratch of the tile LU (inverse diagonal blocks)
   mh::DBuf<double> Lp;     // N*ldL packed strict lower L, columns 0..Q-2 (streamed)
   mh::DBuf<double> Up;     // N*ldL packed strict upper U, columns Q-1..1 (streamed)
   mh::DBuf<double> udiag;  // N*Q   diag(U)

@@ -21,13 +21,26 @@ tables = {"nfe": d + 1, "elem_ufac": prob["elem_face"], "face_elem": prob["face_
           "face_slot": prob["face_slot"], "uidx": prob["uidx"], "F": prob["F"]}
 sys_ = P.condense_arrays(prob["mesh"], prob["A"], None, prob["Be"], prob["R_u"], prob["D"],
                          prob["R_hat"], P.SolverConfig(tol=1e-10), tables=tables)
-ts = []
-for i in range(reps):
-    ms = C.c_float()
-    check(lib.mh_refactorize_local(sys_.handle, C.byref(ms)), "lu")
-    ts.append(ms.value)
 N, Q = prob["N"], prob["Q"]
-best = min(ts[1:] or ts)
-print(f"LU {name} Q={Q} N={N} variant={os.environ.get('MEHDG_LU', 'default')} "
-      f"ms={best:.3f} TFLOP/s={2 / 3 * Q**3 * N / best / 1e9:.2f} all={np.round(ts, 3).tolist()}",
-      flush=True)
+
+
+def run(tag):
+    ts = []
+    for i in range(reps):
+        ms = C.c_float()
+        check(lib.mh_refactorize_local(sys_.handle, C.byref(ms)), "lu")
+        ts.append(ms.value)
+    best = min(ts[1:] or ts)
+    print(f"LU {name} Q={Q} N={N} {tag} ms={best:.3f} "
+          f"TFLOP/s={2 / 3 * Q**3 * N / best / 1e9:.2f} all={np.round(ts, 3).tolist()}", flush=True)
+
+
+run(f"variant={os.environ.get('MEHDG_LU', 'default')}")
+# optional sweep of tuning environment variables, e.g.
+#   python tools/lu_probe.py c2 4 MEHDG_LU_CTAS=1,2,3,4 MEHDG_LU_SCR=0,1
+import itertools  # noqa: E402
+knobs = [(a.split("=")[0], a.split("=")[1].split(",")) for a in sys.argv[3:]]
+for combo in itertools.product(*[v for _, v in knobs]):
+    for (k, _), v in zip(knobs, combo):
+        os.environ[k] = v
+    run(" ".join(f"{k}={v}" for (k, _), v in zip(knobs, combo)))
