@@ -181,6 +181,30 @@ def test_pivoting_blocks(gpu):
     assert rel(P.apply_schur(sys_, prob["uhat"]), o.apply(prob["uhat"])) <= 1e-11
 
 
+@pytest.mark.parametrize("d,n,m,p", [(2, 2, 4, 2), (2, 2, 4, 3), (3, 1, 3, 2), (3, 1, 7, 1),
+                                     (3, 1, 2, 4), (3, 1, 3, 3)])
+@pytest.mark.parametrize("kind", ["gauss", "ties"])
+def test_pivoting_blocks_tile_lu(gpu, d, n, m, p, kind):
+    """Row interchanges in the tile LU (Q = 45, 91, 84, 120 (padded tile), 165, 220):
+    LAPACK pivots bit-exact, including first-index ties (small-integer blocks)."""
+    prob = S.make_problem(d, n, m, p, seed=13)
+    rng = np.random.default_rng(17)
+    if kind == "gauss":
+        prob["A"] = rng.standard_normal(prob["A"].shape)
+    else:
+        prob["A"] = rng.integers(-3, 4, prob["A"].shape).astype(np.float64)
+    sys_, cfg = condense_problem(prob)
+    o = SO.system_from_problem(prob).factorize()
+    lu, piv = P.local_factors(sys_)
+    swaps = 0
+    for e in range(prob["N"]):
+        assert np.array_equal(piv[e], o.lu[e][1])
+        assert np.abs(lu[e] - o.lu[e][0]).max() <= 1e-11 * np.abs(o.lu[e][0]).max()
+        swaps += int((piv[e] != np.arange(prob["Q"])).sum())
+    assert swaps > 0
+    assert rel(P.apply_schur(sys_, prob["uhat"]), o.apply(prob["uhat"])) <= 1e-10
+
+
 def test_singular_local_block_raises_with_id(gpu):
     prob = S.make_problem(2, 2, 1, 1)
     prob["A"] = prob["A"].copy()
@@ -189,6 +213,23 @@ def test_singular_local_block_raises_with_id(gpu):
     with pytest.raises(P.SingularLocalBlock) as ei:
         condense_problem(prob)
     assert ei.value.args[0] == 5
+
+
+@pytest.mark.parametrize("which", ["zero", "repeated_row"])
+def test_singular_local_block_tile_lu(gpu, which):
+    """Tile LU (Q = 91): the singular test min|U_jj| <= 1e-13 max|A| reports the first
+    singular macro; a zero pivot skips the exchange and scaling (dgetf2 info > 0)."""
+    prob = S.make_problem(2, 2, 4, 3, seed=3)
+    prob["A"] = prob["A"].copy()
+    if which == "zero":
+        prob["A"][3] = 0.0
+        bad = 3
+    else:
+        prob["A"][5][7] = prob["A"][5][2]
+        bad = 5
+    with pytest.raises(P.SingularLocalBlock) as ei:
+        condense_problem(prob)
+    assert ei.value.args[0] == bad
 
 
 def test_singular_face_block_raises(gpu):
