@@ -99,12 +99,40 @@ __device__ __forceinline__ double bfrag(double x0, double x1, int kk, int lane) 
   return ((lane >> 2) & 1) ? v1 : v0;
 }
 
+// packed-stream offsets in 32-bit arithmetic (Q <= 256)
+__device__ __forceinline__ int ol32(int j, int Q) { return j * (Q - 1) - j * (j - 1) / 2; }
+__device__ __forceinline__ int ou32(int j, int Q) { return Q * (Q - 1) / 2 - j * (j + 1) / 2; }
+
 // scratch tile (kb, t), t >= kb: packed upper-triangular tile index
 __host__ __device__ constexpr int tri(int kb, int t, int nt) {
   return kb * nt - kb * (kb - 1) / 2 + (t - kb);
 }
 
 __device__ __noinline__ double slow_div(double x, double y) { return x / y; }
+
+__device__ __forceinline__ unsigned hi_abs(double x) {
+  return (unsigned)((uint64_t)__double_as_longlong(x) >> 32) & 0x7fffffffu;
+}
+
+// The reference's test min|U_jj| <= 1e-13 max|A| (schur_solver.py:105-111) from
+// the warp max H of the high words of |a_ij|: max|A| lies in [H:0, H:ffffffff],
+// so the test is decided by the bounds unless dmin falls between them; then the
+// block is re-read for the exact max (practically never).
+__device__ __noinline__ int singular_exact(const double* Ae, int n, double dmin, int lane) {
+  double m = 0.0;
+  for (int i = lane; i < n; i += 32) m = fmax(m, fabs(Ae[i]));
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(kFull, m, o));
+  return dmin <= 1e-13 * fmax(m, 1e-300) ? 1 : 0;
+}
+
+__device__ __forceinline__ int singular_test(const double* Ae, int n, unsigned amh, double dmin,
+                                             int lane) {
+  const double lo = __longlong_as_double((long long)((uint64_t)amh << 32));
+  const double hi = __longlong_as_double((long long)(((uint64_t)amh << 32) | 0xffffffffull));
+  if (dmin <= 1e-13 * fmax(lo, 1e-300)) return 1;
+  if (dmin > 1e-13 * fmax(hi, 1e-300)) return 0;
+  return singular_exact(Ae, n, dmin, lane);
+}
 
 template <int NT>
 struct TileShape {
@@ -169,6 +197,9 @@ __device__ __forceinline__ void factor_panel(double* Pw, int* prow, double* Lpe,
                                              int jb, int lane, uint64_t pol, double& dmin) {
   const int Q = g.Q, c0 = 8 * jb;
   const int ncol = min(8, Q - c0), nrel = Q - c0;
+  bool valid[R];
+#pragma unroll
+  for (int a = 0; a < R; ++a) valid[a] = lane + 32 * a < nrel;
   double P[8][R];
 #pragma unroll
   for (int c = 0; c < 8; ++c)
@@ -178,26 +209,26 @@ __device__ __forceinline__ void factor_panel(double* Pw, int* prow, double* Lpe,
 #pragma unroll
   for (int jj = 0; jj < 8; ++jj) {
     if (jj >= ncol) break;
-    // idamax over relative rows jj..nrel-1 (first index on ties)
-    double bv = 0.0;
-    uint64_t bkey = 0;
+    // idamax over relative rows jj..nrel-1 (first index on ties): per-lane best,
+    // then the warp max of (hi word + 1, lo word) of |a| and the first position
+    double bv = 0.0, babs = -1.0;
     int bpos = INT_MAX;
 #pragma unroll
     for (int a = 0; a < R; ++a) {
-      const int rel = lane + 32 * a;
-      const uint64_t key = (uint64_t)__double_as_longlong(fabs(P[jj][a])) + 1ull;
-      if (rel >= jj && rel < nrel && key > bkey) {
-        bkey = key;
-        bv = P[jj][a];
-        bpos = rel;
+      const double x = P[jj][a], ax = fabs(x);
+      if ((a > 0 || lane >= jj) && valid[a] && ax > babs) {
+        babs = ax;
+        bv = x;
+        bpos = lane + 32 * a;
       }
     }
-    const unsigned hi = (unsigned)(bkey >> 32);
-    const unsigned mhi = __reduce_max_sync(kFull, hi);
-    const unsigned lo = hi == mhi ? (unsigned)bkey : 0u;
-    const unsigned mlo = __reduce_max_sync(kFull, lo);
+    const uint64_t bits = (uint64_t)__double_as_longlong(babs);
+    const unsigned khi = babs < 0.0 ? 0u : (unsigned)(bits >> 32) + 1u;
+    const unsigned mhi = __reduce_max_sync(kFull, khi);
+    const unsigned klo = khi == mhi ? (unsigned)bits : 0u;
+    const unsigned mlo = __reduce_max_sync(kFull, klo);
     const int prel = (int)__reduce_min_sync(
-        kFull, (unsigned)((hi == mhi && (unsigned)bkey == mlo) ? bpos : INT_MAX));
+        kFull, (unsigned)((khi == mhi && (unsigned)bits == mlo) ? bpos : INT_MAX));
     const double pv = __shfl_sync(kFull, bv, prel & 31);
     if (prel != jj && pv != 0.0) {
 #pragma unroll
@@ -237,20 +268,21 @@ __device__ __forceinline__ void factor_panel(double* Pw, int* prow, double* Lpe,
       g.udiag[e * Q + k] = pv;
       g.dinv[e * Q + k] = rcp;
     }
-    dmin = fmin(dmin, fabs(pv));
+    const double apv = fabs(pv);
+    dmin = apv < dmin ? apv : dmin;
   }
   // ---- 4. store L (below the diagonal) and the diagonal block's U
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
     if (c >= ncol) break;
     const int j = c0 + c;
-    double* lcol = Lpe + (off_lower(j, Q) - c - 1);  // + rel
+    double* lcol = Lpe + (ol32(j, Q) - c - 1);  // + rel
 #pragma unroll
     for (int a = 0; a < R; ++a) {
       const int rel = lane + 32 * a;
       if (rel > c && rel < nrel) st_first(lcol + rel, P[c][a], pol);
     }
-    if (lane < c) st_first(Upe + off_upper(j, Q) + c0 + lane, P[c][0], pol);
+    if (lane < c) st_first(Upe + ou32(j, Q) + c0 + lane, P[c][0], pol);
   }
 #pragma unroll
   for (int c = 0; c < 8; ++c)
@@ -303,7 +335,8 @@ __global__ void __launch_bounds__(kTileWarps * 32, TileShape<NT>::kMinBlocks)
     double* Upe = g.Up + e * g.ldL;
     for (int i = lane; i < 32 * R; i += 32) prow[i] = i;
     __syncwarp();
-    double amax = 0.0, dmin = DBL_MAX;
+    unsigned amh = 0;  // max over the block of the high word of |a_ij|
+    double dmin = DBL_MAX;
 
     for (int jb = 0; jb < npanel; ++jb) {
       const int c0 = 8 * jb;
@@ -320,20 +353,12 @@ __global__ void __launch_bounds__(kTileWarps * 32, TileShape<NT>::kMinBlocks)
         const double* src = Ae + prow[vr ? pos : 0] * Q + ca;
         T[t][0] = (vr && v0) ? ld_a(src, apol) : 0.0;
         T[t][1] = (vr && v1) ? ld_a(src + 1, apol) : 0.0;
-        amax = fmax(amax, fmax(fabs(T[t][0]), fabs(T[t][1])));
-      }
-      if (jb + 1 < npanel) {  // next panel's columns of A -> L1 while this one is worked on
-#pragma unroll
-        for (int t = 0; t < NT; ++t) {
-          const int pos = 8 * t + r;
-          if (pos < Q && ca + 8 < Q)
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(Ae + prow[pos] * Q + ca + 8));
-        }
+        amh = max(amh, max(hi_abs(T[t][0]), hi_abs(T[t][1])));
       }
       // ---- 2. left-looking updates with the earlier panels (DMMA)
       {
-        double* U0 = Upe + off_upper(v0 ? ca : 0, Q) + r;
-        double* U1 = Upe + off_upper(v1 ? ca + 1 : 0, Q) + r;
+        double* U0 = Upe + ou32(v0 ? ca : 0, Q) + r;
+        double* U1 = Upe + ou32(v1 ? ca + 1 : 0, Q) + r;
 #pragma unroll
         for (int kb = 0; kb < NT - 1; ++kb) {
           if (kb >= jb) break;
@@ -397,8 +422,8 @@ __global__ void __launch_bounds__(kTileWarps * 32, TileShape<NT>::kMinBlocks)
       Upe[i] = 0.0;
     }
     for (int i = lane; i < Q; i += 32) g.perm[e * Q + i] = prow[i];
-    for (int o = 16; o; o >>= 1) amax = fmax(amax, __shfl_xor_sync(kFull, amax, o));
-    if (lane == 0) g.stat[e] = (dmin <= 1e-13 * fmax(amax, 1e-300)) ? 1 : 0;
+    const int sing = singular_test(Ae, Q * Q, __reduce_max_sync(kFull, amh), dmin, lane);
+    if (lane == 0) g.stat[e] = sing;
     __syncwarp();
   }
 }

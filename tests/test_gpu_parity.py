@@ -232,6 +232,24 @@ def test_singular_local_block_tile_lu(gpu, which):
     assert ei.value.args[0] == bad
 
 
+def test_singular_threshold_exact_at_the_boundary(gpu):
+    """min|U_jj| <= 1e-13 max|A| decided exactly when it is within the kernel's
+    high-word bound on max|A| (the exact re-read path): block 2 sits on the
+    threshold (singular), block 1 one ulp above it (regular)."""
+    prob = S.make_problem(2, 2, 4, 3, seed=3)
+    Q = prob["Q"]
+    A = np.repeat(np.eye(Q)[None], prob["N"], axis=0)
+    M = 1.9999999999  # low word of the bit pattern far from 0 and from 0xffffffff
+    for e in (1, 2):
+        A[e, 0, 0] = M
+    A[2, 5, 5] = 1e-13 * M
+    A[1, 5, 5] = np.nextafter(1e-13 * M, 1.0)
+    prob["A"] = A
+    with pytest.raises(P.SingularLocalBlock) as ei:
+        condense_problem(prob)
+    assert ei.value.args[0] == 2
+
+
 def test_singular_face_block_raises(gpu):
     prob = S.make_problem(2, 2, 1, 1)
     prob["D"] = prob["D"].copy()
