@@ -152,6 +152,14 @@ int mh_apply_host(mh_system* sys, const double* uhat_host, double* w_host);
 int mh_precond_host(mh_system* sys, const double* w_host, double* z_host);
 int mh_rhs_host(mh_system* sys, double* f_host);
 int mh_reconstruct_host(mh_system* sys, const double* uhat_host, double* U_host);
+/* w_i = (D - C A^-1 B) u_i for k host vectors u_i = uhat_host + i*ldu,
+ * w_i = w_host + i*ldw (strides in doubles; 0 reuses one input / overwrites
+ * one output).  The host->device copy of vector i+1 and the device->host copy
+ * of vector i-1 overlap the apply of vector i (two copy streams, two device
+ * buffer pairs); returns when every w_i is in host memory.  Pinned host memory
+ * lets the copies run asynchronously. */
+int mh_apply_host_many(mh_system* sys, int64_t k, const double* uhat_host, int64_t ldu,
+                       double* w_host, int64_t ldw);
 
 /* ---- explicit (matrix-based) Schur, mode "mb" (schur_solver.py:388-420) */
 /* Form S_e = C A^-1 B (nc x nc) per macro on the device; afterwards

@@ -19,7 +19,7 @@ _EXPORTS = {
              "build_structured_macro_mesh", "condense_tables", "mesh_tables"],
     "schur_solver": ["CondensedSystem", "Preconditioner", "SchurOperator", "SingularFaceBlock",
                      "SingularLocalBlock", "Solution", "SolveReport", "SolverConfig",
-                     "WorkerPool", "apply_preconditioner", "apply_schur", "apply_schur_mb",
+                     "WorkerPool", "apply_preconditioner", "apply_schur", "apply_schur_many", "apply_schur_mb",
                      "assemble_schur_explicit", "condense", "condense_arrays",
                      "form_element_schur", "gmres", "local_factors", "reconstruct_interior",
                      "solve", "solve_condensed"],

@@ -69,6 +69,7 @@ SIGNATURES = {
     "mh_apply_precond": [_p, _dp, _dp],
     "mh_reconstruct": [_p, _dp, _dp],
     "mh_apply_host": [_p, _dp, _dp],
+    "mh_apply_host_many": [_p, C.c_int64, _dp, C.c_int64, _dp, C.c_int64],
     "mh_precond_host": [_p, _dp, _dp],
     "mh_rhs_host": [_p, _dp],
     "mh_reconstruct_host": [_p, _dp, _dp],

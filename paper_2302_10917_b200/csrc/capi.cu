@@ -3,6 +3,7 @@
 // to the reference functions (schur_solver.py).
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -122,6 +123,9 @@ extern "C" int mh_create(int device, int nfe, int64_t n_elem, int q, int t, int6
   s->nc = nfe * t;
   s->F = n_face;
   cudaDeviceGetAttribute(&s->max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  if (const char* v = getenv("MEHDG_L2_PERSIST")) {  // tuning experiment: L2 set-aside bytes
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)atoll(v));
+  }
   cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, device);
   cudaError_t e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
   if (e != cudaSuccess) {
@@ -149,6 +153,11 @@ extern "C" int mh_destroy(mh_system* s) {
   for (auto& pr : s->ev_elem) { s->ev_pool.push_back(pr.first); s->ev_pool.push_back(pr.second); }
   for (auto& pr : s->ev_face) { s->ev_pool.push_back(pr.first); s->ev_pool.push_back(pr.second); }
   for (cudaEvent_t e : s->ev_pool) cudaEventDestroy(e);
+  if (s->cin) {
+    cudaStreamDestroy(s->cin);
+    cudaStreamDestroy(s->cout);
+    for (cudaEvent_t e : s->evp) cudaEventDestroy(e);
+  }
   if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
   delete s;
   return MH_OK;
@@ -433,6 +442,55 @@ extern "C" int mh_apply_host(mh_system* s, const double* u, double* w) {
   MH_CHECK(mh_apply(s, s->hin.p, s->hout.p));
   MH_CHECK_CUDA(cudaMemcpyAsync(w, s->hout.p, n * 8, cudaMemcpyDeviceToHost, s->stream));
   MH_CHECK_CUDA(cudaStreamSynchronize(s->stream));
+  return MH_OK;
+}
+
+// k host vectors through the operator with the transfers overlapped: vector i
+// is copied in on one copy stream while vector i-1 is applied on the system
+// stream and vector i-2's result is copied out on another (two device buffer
+// pairs; the copy engines run concurrently with the kernels).  Strides are in
+// doubles; a zero stride reuses one input / overwrites one output.
+extern "C" int mh_apply_host_many(mh_system* s, int64_t k, const double* u, int64_t ldu,
+                                  double* w, int64_t ldw) {
+  MH_CHECK(ready(s));
+  const size_t n = (size_t)(s->F * s->t);
+  if (k < 0 || ldu < 0 || ldw < 0 || (k > 0 && (!u || !w))) {
+    set_error("mh_apply_host_many: bad arguments");
+    return MH_E_ARG;
+  }
+  if (k == 0) return MH_OK;
+  MH_CHECK(host_io(s, 2 * n, 2 * n));
+  if (!s->cin) {
+    MH_CHECK_CUDA(cudaStreamCreateWithFlags(&s->cin, cudaStreamNonBlocking));
+    MH_CHECK_CUDA(cudaStreamCreateWithFlags(&s->cout, cudaStreamNonBlocking));
+    for (int b = 0; b < 7; ++b) MH_CHECK_CUDA(cudaEventCreateWithFlags(&s->evp[b], cudaEventDisableTiming));
+  }
+  cudaEvent_t* ev_in = s->evp;       // [2] copy-in done
+  cudaEvent_t* ev_comp = s->evp + 2; // [2] apply done
+  cudaEvent_t* ev_out = s->evp + 4;  // [2] copy-out done
+  // earlier work on the system stream (which may still read hin / hout) first
+  MH_CHECK_CUDA(cudaEventRecord(s->evp[6], s->stream));
+  MH_CHECK_CUDA(cudaStreamWaitEvent(s->cin, s->evp[6], 0));
+  MH_CHECK_CUDA(cudaStreamWaitEvent(s->cout, s->evp[6], 0));
+  for (int64_t i = 0; i < k; ++i) {
+    const int b = (int)(i & 1);
+    double* ud = s->hin.p + b * n;
+    double* wd = s->hout.p + b * n;
+    if (i >= 2) MH_CHECK_CUDA(cudaStreamWaitEvent(s->cin, ev_comp[b], 0));
+    MH_CHECK_CUDA(cudaMemcpyAsync(ud, u + i * ldu, n * 8, cudaMemcpyHostToDevice, s->cin));
+    MH_CHECK_CUDA(cudaEventRecord(ev_in[b], s->cin));
+    MH_CHECK_CUDA(cudaStreamWaitEvent(s->stream, ev_in[b], 0));
+    if (i >= 2) MH_CHECK_CUDA(cudaStreamWaitEvent(s->stream, ev_out[b], 0));
+    MH_CHECK(mh_apply(s, ud, wd));
+    MH_CHECK_CUDA(cudaEventRecord(ev_comp[b], s->stream));
+    MH_CHECK_CUDA(cudaStreamWaitEvent(s->cout, ev_comp[b], 0));
+    MH_CHECK_CUDA(cudaMemcpyAsync(w + i * ldw, wd, n * 8, cudaMemcpyDeviceToHost, s->cout));
+    MH_CHECK_CUDA(cudaEventRecord(ev_out[b], s->cout));
+  }
+  MH_CHECK_CUDA(cudaStreamSynchronize(s->cout));
+  MH_CHECK_CUDA(cudaStreamSynchronize(s->cin));
+  // the system stream's later work sees hin / hout free again
+  MH_CHECK_CUDA(cudaStreamWaitEvent(s->stream, ev_out[(k - 1) & 1], 0));
   return MH_OK;
 }
 

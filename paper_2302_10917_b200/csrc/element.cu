@@ -28,6 +28,9 @@
 // of four behind one ring-window check, and a group that does not wrap
 // around the ring end is read with immediate-offset shared loads.
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "mh_internal.h"
 #include "stream.cuh"
 
@@ -418,6 +421,7 @@ int launch_rm(mh_system* s, const ElemArgs& a) {
   int per_sm = 0;
   MH_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
   if (per_sm < 1) per_sm = 1;
+  if (const char* v = getenv("MEHDG_ELEM_CTAS")) per_sm = std::max(1, std::min(per_sm, atoi(v)));
   int64_t grid = (int64_t)s->num_sms * per_sm;
   const int64_t need = (s->N + kWPB - 1) / kWPB;
   if (grid > need) grid = need;

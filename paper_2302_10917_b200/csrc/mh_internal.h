@@ -80,6 +80,8 @@ struct mh_system {
   int64_t n_vslot_extra = 0;  // received v-slot segments (multi-GPU)
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  cudaStream_t cin = nullptr, cout = nullptr;  // copy streams of mh_apply_host_many
+  cudaEvent_t evp[7] = {};
   bool have_conn = false, have_blocks = false, factored = false, have_mb = false;
   bool c_is_bt = false;
   int max_smem_optin = 0;

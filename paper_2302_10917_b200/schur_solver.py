@@ -110,7 +110,7 @@ class _Handle:
 
     def __del__(self):
         h = getattr(self, "h", None)
-        if h:
+        if h and lib is not None:  # lib is None during interpreter shutdown
             lib.mh_destroy(h)
             self.h = None
 
@@ -403,6 +403,40 @@ def apply_schur(sys: CondensedSystem, uhat, out=None):
     sys.counters["face_reduce"] += sys.F
     sys.timings["local"] += time.perf_counter() - t0
     return w
+
+
+def apply_schur_many(sys: CondensedSystem, U, out=None, repeat: Optional[int] = None):
+    """The operator on a stack of host vectors U (k x zhat numpy), returning
+    W (k x zhat): the host->device copy of vector i+1 and the device->host copy
+    of vector i-1 overlap the apply of vector i (mh_apply_host_many).  With
+    ``repeat=k`` a single vector U (zhat,) is applied k times into one output
+    (k copies in and out, as a streaming benchmark does).  Pinned host
+    memory (e.g. ``torch.empty(..., pin_memory=True).numpy()``) keeps the
+    copies asynchronous."""
+    U = np.asarray(U)
+    if U.dtype != np.float64 or not U.flags.c_contiguous:
+        raise ValueError("U must be a contiguous float64 array")
+    if repeat is not None:
+        if U.shape != (sys.zhat,):
+            raise ValueError(f"expected a vector of length {sys.zhat} with repeat=")
+        k, ldu = int(repeat), 0
+        shape = (sys.zhat,)
+    else:
+        if U.ndim != 2 or U.shape[1] != sys.zhat:
+            raise ValueError(f"expected a (k, {sys.zhat}) array")
+        k, ldu = U.shape[0], sys.zhat
+        shape = U.shape
+    if out is None:
+        out = np.empty(shape)
+    elif out.shape != shape or out.dtype != np.float64 or not out.flags.c_contiguous:
+        raise ValueError(f"out must be a contiguous float64 array of shape {shape}")
+    t0 = time.perf_counter()
+    check(lib.mh_apply_host_many(sys.handle, k, ptr(U), ldu, ptr(out),
+                                 0 if repeat is not None else sys.zhat), "mh_apply_host_many")
+    sys.counters["macro_apply"] += k * sys.N
+    sys.counters["face_reduce"] += k * sys.F
+    sys.timings["local"] += time.perf_counter() - t0
+    return out
 
 
 def apply_preconditioner(sys: CondensedSystem, w):

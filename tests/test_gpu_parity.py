@@ -96,6 +96,22 @@ def test_apply_deterministic_and_linear(c1):
     assert np.abs(lhs - rhs).max() < 1e-10 * max(1.0, np.abs(rhs).max())
 
 
+def test_apply_schur_many_matches_single_applies(c1):
+    """mh_apply_host_many (copies overlapped with the applies) is bitwise the
+    per-vector apply, for a stack of vectors and for the repeat form."""
+    _, sys_, _ = c1
+    rng = np.random.default_rng(4)
+    U = rng.standard_normal((5, sys_.zhat))
+    W = P.apply_schur_many(sys_, U)
+    for i in range(5):
+        assert np.array_equal(W[i], P.apply_schur(sys_, U[i]))
+    w1 = P.apply_schur_many(sys_, U[2].copy(), repeat=7)
+    assert np.array_equal(w1, W[2])
+    assert P.apply_schur_many(sys_, U[:0]).shape == (0, sys_.zhat)
+    with pytest.raises(ValueError):
+        P.apply_schur_many(sys_, U[:, :-1])
+
+
 def test_device_tensor_path_matches_host_path(c1):
     import torch
 
