@@ -161,6 +161,40 @@ int mh_reconstruct_host(mh_system* sys, const double* uhat_host, double* U_host)
 int mh_apply_host_many(mh_system* sys, int64_t k, const double* uhat_host, int64_t ldu,
                        double* w_host, int64_t ldw);
 
+/* ---- device assembly of the 2-D HDG blocks (assembly.py:170-322) ----------
+ * Reference-element tables (device pointers) of a conforming structured mesh,
+ * built by paper_2302_10917_b200/fem.py; nloc = 3 Q, nc = 3 t. */
+typedef struct {
+  int32_t m, p, Q, nb, t, nq, ncell, nfq, nffq, supg, supg_plus;
+  double kappa, ax, ay;
+  const double* qw;         /* nq quadrature weights on the reference triangle */
+  const double* val;        /* nq x nb basis values */
+  const double* gref;       /* nq x nb x 2 reference gradients */
+  const double* href;       /* nq x nb x 2 x 2 reference Hessians (SUPG) */
+  const int32_t* cell_kind; /* ncell: 0 "up", 1 "down" (mesh.py:71-77 order) */
+  const int32_t* cell_map;  /* ncell x nb sub-cell dof -> patch dof */
+  const int32_t* edge_nodes;/* 3 x t patch dofs along each macro edge */
+  const double* fw;         /* nfq weights of assemble_macro's face rule */
+  const double* th_fwd;     /* nfq x t macro-edge trace basis at t = s */
+  const double* th_rev;     /* nfq x t ... at t = 1 - s */
+  const double* ps;         /* nfq x t face trace basis */
+  const double* ffw;        /* nffq weights of assemble_face's rule */
+  const double* fps;        /* nffq x t */
+} mh_hdg2d_tables;
+/* assemble_macro for N macros: verts[N*3*2], edge_rev[N*3] (1 when the face
+ * parameter runs against the macro edge, t0 = 1), edge_dirichlet[N*3] (row of
+ * ghat[nD*t] for a Dirichlet face, else -1), fq[N*ncell*nq] (f at the physical
+ * quadrature points).  Outputs (device, row-major): A[N*nloc*nloc],
+ * B[N*nloc*nc] (op.B), C[N*nc*nloc] (op.C), Ru[N*nloc].  stream: cudaStream_t. */
+int mh_assemble_macros_2d(const mh_hdg2d_tables* tab, int64_t N, const double* verts,
+                          const int8_t* edge_rev, const int32_t* edge_dirichlet,
+                          const double* ghat, const double* fq, double* A, double* B, double* C,
+                          double* Ru, void* stream);
+/* assemble_face's D block for F faces: face_sides[F*4] = (left macro, left
+ * edge, right macro or -1, right edge); D[F*t*t] row-major. */
+int mh_assemble_faces_2d(const mh_hdg2d_tables* tab, int64_t F, const double* verts,
+                         const int32_t* face_sides, double* D, void* stream);
+
 /* ---- explicit (matrix-based) Schur, mode "mb" (schur_solver.py:388-420) */
 /* Form S_e = C A^-1 B (nc x nc) per macro on the device; afterwards
  * mh_apply_mb computes w = D uhat - sum_e S_e uhat_e with the same face

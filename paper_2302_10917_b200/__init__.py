@@ -13,7 +13,8 @@ from importlib import import_module
 __version__ = "0.1.0"
 
 _EXPORTS = {
-    "assembly": ["FaceOperator", "LocalOperators", "operators_from_problem"],
+    "assembly": ["DeviceBlocks", "FaceOperator", "LocalOperators", "ProblemData",
+                 "StabilizationConfig", "assemble_system_device", "operators_from_problem"],
     "io": ["export_text", "read_csv", "rows_to_csv", "write_csv"],
     "mesh": ["FaceSide", "MacroElement", "SkeletonFace", "StructuredMacroMesh",
              "build_structured_macro_mesh", "condense_tables", "mesh_tables"],

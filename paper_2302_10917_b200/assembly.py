@@ -1,14 +1,23 @@
-"""Hot-path data contract of ``mehdg.assembly`` (assembly.py:63-82).
+"""``mehdg.assembly`` on the B200 path.
 
-Only the block containers cross the drop-in boundary; FEM quadrature
-assembly itself is outside the B200 path.
+* The block containers of the drop-in boundary (assembly.py:63-82).
+* Device assembly of the 2-D HDG blocks:
+  ``assemble_system_device`` is ``assemble_system`` (schur_solver.py:482-492)
+  with assemble_macro / assemble_face (assembly.py:170-322) computed by the
+  csrc/assembly.cu kernels.  The host builds the reference-element tables
+  (fem.py), evaluates the problem data (Python callables) at the quadrature
+  points and projects the Dirichlet data; the blocks never leave the device.
 """
 
 from __future__ import annotations
 
+import ctypes as C
 from dataclasses import dataclass
+from typing import Callable, Optional
 
 import numpy as np
+
+from . import fem
 
 
 @dataclass
@@ -56,3 +65,177 @@ def operators_from_problem(prob: dict):
             face_ops[fid] = FaceOperator(face_id=fid, D=prob["D"][u], R_hat=prob["R_hat"][u],
                                          tag=str(mesh.face_tag[fid]))
     return local_ops, face_ops
+
+
+@dataclass
+class ProblemData:
+    """assembly.py:36-50: constant-velocity advection-diffusion data; f, g_D, g_N
+    map (npts, 2) points to (npts,) values."""
+
+    a: np.ndarray
+    kappa: float
+    f: Callable
+    g_D: Callable
+    g_N: Optional[Callable] = None
+
+    def __post_init__(self):
+        self.a = np.asarray(self.a, dtype=float)
+        if self.kappa <= 0:
+            raise ValueError("kappa must be positive")
+
+
+@dataclass
+class StabilizationConfig:
+    """assembly.py:53-60."""
+
+    supg: bool = False
+    supg_variant: str = "classical-minus"  # or "paper-plus"
+
+    def __post_init__(self):
+        if self.supg_variant not in ("classical-minus", "paper-plus"):
+            raise ValueError(f"unknown supg variant {self.supg_variant!r}")
+
+
+class _Tables(C.Structure):
+    """mh_hdg2d_tables (include/mehdg_b200.h)."""
+
+    _fields_ = [(n, C.c_int32) for n in ("m", "p", "Q", "nb", "t", "nq", "ncell", "nfq",
+                                         "nffq", "supg", "supg_plus")] + \
+               [(n, C.c_double) for n in ("kappa", "ax", "ay")] + \
+               [(n, C.c_void_p) for n in ("qw", "val", "gref", "href", "cell_kind", "cell_map",
+                                          "edge_nodes", "fw", "th_fwd", "th_rev", "ps", "ffw",
+                                          "fps")]
+
+
+@dataclass
+class DeviceBlocks:
+    """Assembled blocks on the device (torch float64 CUDA tensors), in the
+    layouts of LocalOperators / FaceOperator: A (N, nloc, nloc), B (N, nloc, nc)
+    = op.B, C (N, nc, nloc) = op.C, R_u (N, nloc); D (F, t, t), R_hat (F, t) in
+    unknown-face order."""
+
+    A: object
+    B: object
+    C: object
+    R_u: object
+    D: object
+    R_hat: object
+    nloc: int
+    t: int
+    p: int
+    m: int
+    tables: dict
+
+
+def _side_orientation(mesh, verts: np.ndarray) -> np.ndarray:
+    """(N, 3) int8: 1 where the face parameter runs against macro edge k
+    (side t0 = 1; mesh.py:228-233 with the canonical lexicographic face vertex
+    order, mesh.py:222-223)."""
+    N = verts.shape[0]
+    rev = np.zeros((N, 3), np.int8)
+    if hasattr(mesh, "vertices_lattice"):  # exact integer lattice order
+        lat = mesh.vertices_lattice[mesh.elem_verts]  # (N, 3, 2)
+        for k, (a, b) in enumerate(fem.EDGE_VERTS):
+            pa, pb = lat[:, a], lat[:, b]
+            rev[:, k] = (pa[:, 0] > pb[:, 0]) | ((pa[:, 0] == pb[:, 0]) & (pa[:, 1] > pb[:, 1]))
+        return rev
+    for face in mesh.skeleton:  # the reference MacroMesh: its FaceSide t0 / t1
+        for side in face.sides():
+            rev[side.macro, side.edge] = 1 if side.t0 > side.t1 else 0
+    return rev
+
+
+def _face_verts(mesh, fids: np.ndarray) -> np.ndarray:
+    if hasattr(mesh, "face_verts"):
+        return mesh.vertices[mesh.face_verts[fids]]
+    return np.stack([np.asarray(mesh.skeleton[int(f)].verts, float) for f in fids]) \
+        if len(fids) else np.zeros((0, 2, 2))
+
+
+def assemble_system_device(mesh, problem: ProblemData, stab: StabilizationConfig, p: int,
+                           quad_degree: Optional[int] = None, device: int = 0,
+                           tables: Optional[dict] = None) -> DeviceBlocks:
+    """assemble_system (schur_solver.py:482-492) on the device, for a conforming
+    2-D structured macro mesh (ours or the reference's)."""
+    from . import _lib
+    from ._lib import check, lib
+    from .mesh import condense_tables, mesh_tables
+    import torch
+
+    _lib.require_gpu()
+    if getattr(mesh, "d", 2) != 2:
+        raise NotImplementedError("the HDG block assembly is two-dimensional (assembly.py)")
+    ms = {int(e.m) for e in mesh.macro_elements} if not hasattr(mesh, "m") else {int(mesh.m)}
+    if len(ms) != 1:
+        raise NotImplementedError("mixed macro subdivisions (adaptive meshes) are not on the "
+                                  "B200 path (SURVEY.md 8(f) row 4)")
+    m = ms.pop()
+    if tables is None:
+        tables = mesh_tables(mesh)
+        tables.update(condense_tables(tables))
+    if quad_degree is None:
+        quad_degree = 2 * p + 2 if stab.supg else 2 * p + 1  # assembly.py:188-189
+    tab = fem.asm_tables(m, p, quad_degree)
+    dev = torch.device(f"cuda:{device}")
+    verts = fem.macro_geometry(mesh)
+    N = verts.shape[0]
+    Q, t = tab.Q, tab.t
+    nloc, nc = 3 * Q, 3 * t
+
+    def d(x, dtype=torch.float64):
+        return torch.as_tensor(np.ascontiguousarray(x), dtype=dtype, device=dev)
+
+    # problem data at the quadrature points (host; the data are Python callables)
+    pts = fem.quad_points(verts, tab)
+    fq = np.asarray(problem.f(pts.reshape(-1, 2)), dtype=float).reshape(pts.shape[:3])
+    face_tag = np.array([str(tg) for tg in (mesh.face_tag if hasattr(mesh, "face_tag")
+                                            else [f.tag for f in mesh.skeleton])])
+    elem_face = np.asarray(tables["elem_face"])
+    dfaces = np.nonzero(face_tag == "D")[0]
+    drow = np.full(face_tag.size, -1, np.int32)
+    drow[dfaces] = np.arange(dfaces.size, dtype=np.int32)
+    edge_dir = drow[elem_face]
+    ghat = fem.dirichlet_projection(_face_verts(mesh, dfaces), problem.g_D, p, m) \
+        if dfaces.size else np.zeros((1, t))
+    rev = _side_orientation(mesh, verts)
+
+    keep = dict(qw=d(tab.qw), val=d(tab.val), gref=d(tab.gref), href=d(tab.href),
+                cell_kind=d(tab.cell_kind, torch.int32), cell_map=d(tab.cell_map, torch.int32),
+                edge_nodes=d(tab.edge_nodes, torch.int32), fw=d(tab.fw), th_fwd=d(tab.th_fwd),
+                th_rev=d(tab.th_rev), ps=d(tab.ps), ffw=d(tab.ffw), fps=d(tab.fps))
+    T = _Tables(m=m, p=p, Q=Q, nb=tab.nb, t=t, nq=tab.qw.size, ncell=len(tab.cell_kind),
+                nfq=tab.fw.size, nffq=tab.ffw.size, supg=int(stab.supg),
+                supg_plus=int(stab.supg_variant == "paper-plus"), kappa=float(problem.kappa),
+                ax=float(problem.a[0]), ay=float(problem.a[1]),
+                **{k: v.data_ptr() for k, v in keep.items()})
+    A = torch.empty((N, nloc, nloc), dtype=torch.float64, device=dev)
+    B = torch.empty((N, nloc, nc), dtype=torch.float64, device=dev)
+    Cm = torch.empty((N, nc, nloc), dtype=torch.float64, device=dev)
+    Ru = torch.empty((N, nloc), dtype=torch.float64, device=dev)
+    verts_d, rev_d, dir_d = d(verts), d(rev, torch.int8), d(edge_dir, torch.int32)
+    ghat_d, fq_d = d(ghat), d(fq)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    check(lib.mh_assemble_macros_2d(C.addressof(T), N, verts_d.data_ptr(), rev_d.data_ptr(),
+                                    dir_d.data_ptr(), ghat_d.data_ptr(), fq_d.data_ptr(),
+                                    A.data_ptr(), B.data_ptr(), Cm.data_ptr(), Ru.data_ptr(),
+                                    stream), "mh_assemble_macros_2d")
+    # face blocks in unknown-face order (the order of condense's offsets)
+    uidx = np.asarray(tables["uidx"])
+    ufaces = np.nonzero(uidx >= 0)[0]
+    ufaces = ufaces[np.argsort(uidx[ufaces])]
+    F = ufaces.size
+    sides = np.concatenate((np.asarray(tables["face_left"])[ufaces],
+                            np.asarray(tables["face_right"])[ufaces]), axis=1).astype(np.int32)
+    D = torch.empty((F, t, t), dtype=torch.float64, device=dev)
+    sides_d = d(sides, torch.int32)
+    check(lib.mh_assemble_faces_2d(C.addressof(T), F, verts_d.data_ptr(), sides_d.data_ptr(),
+                                   D.data_ptr(), stream), "mh_assemble_faces_2d")
+    Rh = np.zeros((F, t))
+    nfaces = np.nonzero(face_tag[ufaces] == "N")[0]
+    if nfaces.size:
+        if problem.g_N is None:
+            raise ValueError("Neumann face present but g_N not provided")
+        Rh[nfaces] = fem.neumann_rhs(_face_verts(mesh, ufaces[nfaces]), problem.g_N, p, m)
+    torch.cuda.current_stream(dev).synchronize()
+    return DeviceBlocks(A=A, B=B, C=Cm, R_u=Ru, D=D, R_hat=d(Rh), nloc=nloc, t=t, p=p, m=m,
+                        tables=tables)

@@ -276,8 +276,9 @@ def condense_arrays(mesh, A, B, Cm, R_u, D, R_hat, config: SolverConfig, *, p: i
         tables = mesh_tables(mesh)
         tables.update(condense_tables(tables))
     tables = dict(tables)
-    if face_ops is None:
-        tables["D"] = D  # host face blocks for assemble_schur_explicit
+    on_device = _is_torch(A)
+    if face_ops is None:  # host face blocks for assemble_schur_explicit
+        tables["D"] = D.detach().cpu().numpy() if on_device else D
     N, Q = A.shape[0], A.shape[1]
     nfe = tables["nfe"]
     F = int(tables["F"]) if "F" in tables else int((tables["uidx"] >= 0).sum())
@@ -290,12 +291,20 @@ def condense_arrays(mesh, A, B, Cm, R_u, D, R_hat, config: SolverConfig, *, p: i
                                      ptr(np.ascontiguousarray(tables["face_slot"], np.int32))),
           "mh_upload_connectivity")
 
-    def c64(x):
-        return None if x is None else np.ascontiguousarray(x, dtype=np.float64)
+    if on_device:  # blocks assembled on the device (assemble_system_device)
+        def dp(x):
+            return None if x is None else x.contiguous().data_ptr()
 
-    A_, B_, C_, Ru_, D_, Rh_ = c64(A), c64(B), c64(Cm), c64(R_u), c64(D), c64(R_hat)
-    check(lib.mh_upload_blocks(h.h, ptr(A_), ptr(B_), ptr(C_), ptr(Ru_), ptr(D_), ptr(Rh_)),
-          "mh_upload_blocks")
+        keep = [x.contiguous() if x is not None else None for x in (A, B, Cm, R_u, D, R_hat)]
+        check(lib.mh_upload_blocks_device(h.h, *[dp(x) for x in keep]), "mh_upload_blocks_device")
+        torch.cuda.current_stream(dev).synchronize()
+    else:
+        def c64(x):
+            return None if x is None else np.ascontiguousarray(x, dtype=np.float64)
+
+        A_, B_, C_, Ru_, D_, Rh_ = c64(A), c64(B), c64(Cm), c64(R_u), c64(D), c64(R_hat)
+        check(lib.mh_upload_blocks(h.h, ptr(A_), ptr(B_), ptr(C_), ptr(Ru_), ptr(D_), ptr(Rh_)),
+              "mh_upload_blocks")
     fm, ff = C.c_int32(-1), C.c_int32(-1)
     kinds = np.empty(F, np.int8)
     lu_ms = C.c_float(0.0)
@@ -723,13 +732,22 @@ def solve_condensed(sys: CondensedSystem, config: SolverConfig, t_init: float = 
 
 
 def solve(mesh, problem, stab, config: SolverConfig, p: int, assemble: Optional[Callable] = None):
-    """schur_solver.py:495-541.  Block assembly (assembly.py) is not on the
-    B200 path; pass ``assemble(mesh, problem, stab, p) -> (local_ops, face_ops)``
-    (e.g. the reference's ``assemble_system``)."""
+    """schur_solver.py:495-541: assemble, condense, GMRES on the trace system,
+    reconstruct.  By default the blocks are assembled on the device
+    (assembly.assemble_system_device, 2-D) and never leave it; a callable
+    ``assemble(mesh, problem, stab, p) -> (local_ops, face_ops)`` (e.g. the
+    reference's ``assemble_system``) takes the host path instead."""
     if assemble is None:
-        raise NotImplementedError(
-            "FEM block assembly is outside the B200 hot path (SURVEY.md 8(f) row 2); "
-            "pass assemble=callable returning (local_ops, face_ops)")
+        from .assembly import assemble_system_device
+
+        t0 = time.perf_counter()
+        blk = assemble_system_device(mesh, problem, stab, p, device=config.device)
+        t_asm = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        sys = condense_arrays(mesh, blk.A, blk.B, blk.C, blk.R_u, blk.D, blk.R_hat, config,
+                              p=p, tables=blk.tables)
+        sys.timings["assemble"] = t_asm
+        return solve_condensed(sys, config, t_init=time.perf_counter() - t0)
     local_ops, face_ops = assemble(mesh, problem, stab, p)
     t0 = time.perf_counter()
     sys = condense(mesh, local_ops, face_ops, config)

@@ -152,13 +152,30 @@ def run_reference(name, full: bool, gmres_tol=1e-10):
           info["iterations"], info["converged"])
 
 
-def run_real(n=2, m=2, p=2):
-    """Reference assembly (tanh benchmark) -> blocks + reference results."""
+def _neumann_left(x):
+    return "N" if x[0] < 1e-12 else "D"
+
+
+def _g_neumann(x):
+    x = np.atleast_2d(x)
+    return np.sin(3.0 * x[:, 1]) + 0.5 * x[:, 0]
+
+
+def run_real(n=2, m=2, p=2, supg=None, neumann=False, tag=""):
+    """Reference assembly (tanh benchmark) -> blocks + reference results.
+    supg: None or the SUPG variant; neumann: left side of the square tagged "N"
+    with g_N = sin(3y) + x/2."""
     case = make_benchmark("tanh", 0.4, (1.0, 1.0))
-    mesh = R_mesh.build_structured_macro_mesh(2, n, m)
+    tagger = _neumann_left if neumann else None
+    mesh = R_mesh.build_structured_macro_mesh(2, n, m, boundary_tagger=tagger)
+    problem = case.problem()
+    if neumann:
+        problem = R_asm.ProblemData(a=problem.a, kappa=problem.kappa, f=problem.f,
+                                    g_D=problem.g_D, g_N=_g_neumann)
+    stab = R_asm.StabilizationConfig(supg=supg is not None,
+                                     supg_variant=supg or "classical-minus")
     pool = R.WorkerPool(1)
-    local_ops, face_ops = R.assemble_system(mesh, case.problem(), R_asm.StabilizationConfig(), p,
-                                            pool)
+    local_ops, face_ops = R.assemble_system(mesh, problem, stab, p, pool)
     cfg = R.SolverConfig(tol=1e-12)
     sys_ = R.condense(mesh, local_ops, face_ops, cfg, pool=pool)
     rng = np.random.default_rng(3)
@@ -174,17 +191,20 @@ def run_real(n=2, m=2, p=2):
         slot_faces=np.array([[fid for fid, _ in o.face_slots] for o in local_ops]),
         f=sys_.f_vec, xs=xs, w=np.stack([R.apply_schur(sys_, v) for v in xs]),
         z=np.stack([R.apply_preconditioner(sys_, v) for v in xs]),
-        lu=np.stack([o.lu[1][0] for o in local_ops]), piv=np.stack([o.lu[1][1] for o in local_ops]),
+        lu=np.stack([o.lu[1][0] for o in local_ops]) if local_ops[0].storage == "dense"
+        else np.zeros(0),
+        piv=np.stack([o.lu[1][1] for o in local_ops]) if local_ops[0].storage == "dense"
+        else np.zeros(0),
         face_kinds=np.array([{"chol-neg": 0, "chol-pos": 1, "lu": 2}[face_ops[f].factor_kind]
                              for f in sorted(face_ops)]),
-        n=n, m=m, p=p)
+        n=n, m=m, p=p, supg=np.array(supg or ""), neumann=neumann,
+        face_tags=np.array([face_ops[f].tag for f in sorted(face_ops)]))
     x, info = R.gmres(lambda v: R.apply_schur(sys_, v), sys_.f_vec, cfg,
                       precond=lambda v: R.apply_preconditioner(sys_, v))
     out.update(x=x, iterations=info["iterations"], history=np.array(info["residual_history"]),
                U=np.stack(R.reconstruct_interior(sys_, x)))
-    np.savez_compressed(HERE / f"real_tanh_n{n}m{m}p{p}.npz", **out)
-    print("real", n, m, p, "zhat", sys_.zhat, "its", info["iterations"],
-          "swaps", int(sum((o.lu[1][1] != np.arange(o.lu[1][1].size)).sum() for o in local_ops)))
+    np.savez_compressed(HERE / f"real_tanh_n{n}m{m}p{p}{tag}.npz", **out)
+    print("real", n, m, p, tag, "zhat", sys_.zhat, "its", info["iterations"])
 
 
 if __name__ == "__main__":
@@ -196,6 +216,11 @@ if __name__ == "__main__":
     if "real" in which:
         run_real(2, 2, 2)
         run_real(3, 1, 3)
+    if "asm" in which:  # device-assembly fixtures
+        run_real(2, 2, 2, supg="classical-minus", tag="_supg")
+        run_real(2, 2, 3, supg="paper-plus", tag="_supgplus")
+        run_real(2, 3, 2, tag="")
+        run_real(2, 2, 2, neumann=True, tag="_neumann")
     if "c2" in which:
         run_reference("c2", full=False)
     if "c3" in which:

@@ -423,5 +423,3 @@ def test_host_factors_and_solve_driver(gpu):
     assert rec["converged"] and abs(rec["iterations"] - int(g["iterations"])) <= 1
     assert rel(sol.uhat, g["x"]) <= SOLVE_TOL
     assert rel(np.stack(sol.local), g["U"]) <= SOLVE_TOL
-    with pytest.raises(NotImplementedError):
-        P.solve(mesh, None, None, P.SolverConfig(), p)
