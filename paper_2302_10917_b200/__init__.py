@@ -14,7 +14,8 @@ __version__ = "0.1.0"
 
 _EXPORTS = {
     "assembly": ["DeviceBlocks", "FaceOperator", "LocalOperators", "ProblemData",
-                 "StabilizationConfig", "assemble_system_device", "operators_from_problem"],
+                 "StabilizationConfig", "assemble_system_device", "manufactured_tanh",
+                 "operators_from_problem"],
     "io": ["export_text", "read_csv", "rows_to_csv", "write_csv"],
     "mesh": ["FaceSide", "MacroElement", "SkeletonFace", "StructuredMacroMesh",
              "build_structured_macro_mesh", "condense_tables", "mesh_tables"],

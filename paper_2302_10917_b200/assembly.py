@@ -96,6 +96,30 @@ class StabilizationConfig:
             raise ValueError(f"unknown supg variant {self.supg_variant!r}")
 
 
+def manufactured_tanh(kappa: float = 0.4, a=(1.0, 1.0), g_N: Optional[Callable] = None):
+    """The reference's "tanh" manufactured case (mehdg/bench.py:46-70): interior
+    layer u = (1 + tanh((y - 2x + 0.4) / kappa)) / 2 on the unit square."""
+    if kappa <= 0:
+        raise ValueError("kappa must be positive")
+    k = float(kappa)
+    ax, ay = float(a[0]), float(a[1])
+
+    def sech2(z):
+        return 1.0 / np.cosh(np.clip(z, -350.0, 350.0)) ** 2
+
+    def u_exact(x):
+        x = np.atleast_2d(x)
+        return 0.5 * (1.0 + np.tanh((x[:, 1] - 2.0 * x[:, 0] + 0.4) / k))
+
+    def f(x):
+        x = np.atleast_2d(x)
+        z = (x[:, 1] - 2.0 * x[:, 0] + 0.4) / k
+        s2 = sech2(z)
+        return 0.5 * s2 * (ay - 2.0 * ax) / k - k * (-5.0 * s2 * np.tanh(z) / k ** 2)
+
+    return ProblemData(a=np.array([ax, ay]), kappa=k, f=f, g_D=u_exact, g_N=g_N)
+
+
 class _Tables(C.Structure):
     """mh_hdg2d_tables (include/mehdg_b200.h)."""
 
@@ -154,9 +178,15 @@ def _face_verts(mesh, fids: np.ndarray) -> np.ndarray:
 
 def assemble_system_device(mesh, problem: ProblemData, stab: StabilizationConfig, p: int,
                            quad_degree: Optional[int] = None, device: int = 0,
-                           tables: Optional[dict] = None) -> DeviceBlocks:
+                           tables: Optional[dict] = None,
+                           timings: Optional[dict] = None) -> DeviceBlocks:
     """assemble_system (schur_solver.py:482-492) on the device, for a conforming
-    2-D structured macro mesh (ours or the reference's)."""
+    2-D structured macro mesh (ours or the reference's).  ``timings`` (optional
+    dict) receives host_s (tables, data evaluation, uploads) and kernel_ms (the
+    two assembly kernels, CUDA events)."""
+    import time as _time
+
+    t_host0 = _time.perf_counter()
     from . import _lib
     from ._lib import check, lib
     from .mesh import condense_tables, mesh_tables
@@ -215,11 +245,7 @@ def assemble_system_device(mesh, problem: ProblemData, stab: StabilizationConfig
     verts_d, rev_d, dir_d = d(verts), d(rev, torch.int8), d(edge_dir, torch.int32)
     ghat_d, fq_d = d(ghat), d(fq)
     stream = torch.cuda.current_stream(dev).cuda_stream
-    check(lib.mh_assemble_macros_2d(C.addressof(T), N, verts_d.data_ptr(), rev_d.data_ptr(),
-                                    dir_d.data_ptr(), ghat_d.data_ptr(), fq_d.data_ptr(),
-                                    A.data_ptr(), B.data_ptr(), Cm.data_ptr(), Ru.data_ptr(),
-                                    stream), "mh_assemble_macros_2d")
-    # face blocks in unknown-face order (the order of condense's offsets)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     uidx = np.asarray(tables["uidx"])
     ufaces = np.nonzero(uidx >= 0)[0]
     ufaces = ufaces[np.argsort(uidx[ufaces])]
@@ -228,8 +254,16 @@ def assemble_system_device(mesh, problem: ProblemData, stab: StabilizationConfig
                             np.asarray(tables["face_right"])[ufaces]), axis=1).astype(np.int32)
     D = torch.empty((F, t, t), dtype=torch.float64, device=dev)
     sides_d = d(sides, torch.int32)
+    t_host = _time.perf_counter() - t_host0
+    ev0.record(torch.cuda.current_stream(dev))
+    check(lib.mh_assemble_macros_2d(C.addressof(T), N, verts_d.data_ptr(), rev_d.data_ptr(),
+                                    dir_d.data_ptr(), ghat_d.data_ptr(), fq_d.data_ptr(),
+                                    A.data_ptr(), B.data_ptr(), Cm.data_ptr(), Ru.data_ptr(),
+                                    stream), "mh_assemble_macros_2d")
+    # face blocks in unknown-face order (the order of condense's offsets)
     check(lib.mh_assemble_faces_2d(C.addressof(T), F, verts_d.data_ptr(), sides_d.data_ptr(),
                                    D.data_ptr(), stream), "mh_assemble_faces_2d")
+    ev1.record(torch.cuda.current_stream(dev))
     Rh = np.zeros((F, t))
     nfaces = np.nonzero(face_tag[ufaces] == "N")[0]
     if nfaces.size:
@@ -237,5 +271,8 @@ def assemble_system_device(mesh, problem: ProblemData, stab: StabilizationConfig
             raise ValueError("Neumann face present but g_N not provided")
         Rh[nfaces] = fem.neumann_rhs(_face_verts(mesh, ufaces[nfaces]), problem.g_N, p, m)
     torch.cuda.current_stream(dev).synchronize()
+    if timings is not None:
+        timings["host_s"] = t_host
+        timings["kernel_ms"] = ev0.elapsed_time(ev1)
     return DeviceBlocks(A=A, B=B, C=Cm, R_u=Ru, D=D, R_hat=d(Rh), nloc=nloc, t=t, p=p, m=m,
                         tables=tables)

@@ -9,8 +9,8 @@ import numpy as np
 import pytest
 
 import paper_2302_10917_b200 as P
-from paper_2302_10917_b200.assembly import (ProblemData, StabilizationConfig,
-                                            assemble_system_device)
+from paper_2302_10917_b200.assembly import (StabilizationConfig, assemble_system_device,
+                                            manufactured_tanh)
 from conftest import golden, rel
 
 pytestmark = pytest.mark.gpu
@@ -19,29 +19,14 @@ BLOCK_TOL = 1e-12   # assembled entries, relative to the block's max |entry|
 SOLVE_TOL = 1e-9    # converged traces / interior unknowns (north_star)
 
 
-def tanh_problem(kappa=0.4, a=(1.0, 1.0), neumann=False):
-    """The reference's "tanh" manufactured case (mehdg/bench.py:46-70)."""
-    k = kappa
-    ax, ay = a
-
-    def sech2(z):
-        return 1.0 / np.cosh(np.clip(z, -350.0, 350.0)) ** 2
-
-    def u_exact(x):
-        x = np.atleast_2d(x)
-        return 0.5 * (1.0 + np.tanh((x[:, 1] - 2.0 * x[:, 0] + 0.4) / k))
-
-    def f(x):
-        x = np.atleast_2d(x)
-        z = (x[:, 1] - 2.0 * x[:, 0] + 0.4) / k
-        s2 = sech2(z)
-        return 0.5 * s2 * (ay - 2.0 * ax) / k - k * (-5.0 * s2 * np.tanh(z) / k ** 2)
-
-    def g_n(x):  # the fixture's Neumann data (make_golden.py)
+def tanh_problem(neumann=False):
+    """The fixtures' problem: the reference's tanh case (kappa 0.4, a = (1, 1)) and,
+    for the Neumann fixture, g_N = sin(3y) + x/2 (make_golden.py)."""
+    def g_n(x):
         x = np.atleast_2d(x)
         return np.sin(3.0 * x[:, 1]) + 0.5 * x[:, 0]
 
-    return ProblemData(a=np.array(a), kappa=k, f=f, g_D=u_exact, g_N=g_n if neumann else None)
+    return manufactured_tanh(0.4, (1.0, 1.0), g_N=g_n if neumann else None)
 
 
 FIXTURES = ["real_tanh_n2m2p2.npz", "real_tanh_n3m1p3.npz", "real_tanh_n2m3p2.npz",

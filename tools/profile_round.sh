@@ -6,16 +6,16 @@ out=gpurun_out/prof
 mkdir -p $out
 python bench.py > $out/bench_c2.json 2> $out/bench_c2.err
 for c in c3 c5n20 c4; do
-  python bench.py --config $c --steps 50 --warmup 5 --no-cpu-baseline --no-mb > $out/bench_$c.json 2> $out/bench_$c.err
+  python bench.py --config $c --steps 50 --warmup 5 --no-cpu-baseline --no-mb --no-asm > $out/bench_$c.json 2> $out/bench_$c.err
 done
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches_c2.csv \
-  python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-mb > $out/ncu_launch.log 2>&1
+  python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-mb --no-asm > $out/ncu_launch.log 2>&1
 ncu --set full --import-source on --clock-control none -k element_kernel -s 1 -c 1 \
-  -o $out/element_c2 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-mb > $out/ncu_el.log 2>&1
+  -o $out/element_c2 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-mb --no-asm > $out/ncu_el.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:"face_small|face_reduce" -c 2 \
-  -o $out/face_c2 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-mb > $out/ncu_face.log 2>&1
+  -o $out/face_c2 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-mb --no-asm > $out/ncu_face.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:lu_tile -c 1 \
   -o $out/lu_c2 python tools/lu_probe.py c2 1 > $out/ncu_lu.log 2>&1
 ncu --set full --import-source on --clock-control none -k element_kernel -s 1 -c 1 \
-  -o $out/element_c3 python bench.py --config c3 --steps 3 --warmup 3 --no-cpu-baseline --no-mb > $out/ncu_el3.log 2>&1
+  -o $out/element_c3 python bench.py --config c3 --steps 3 --warmup 3 --no-cpu-baseline --no-mb --no-asm > $out/ncu_el3.log 2>&1
 ls -la $out
