@@ -207,6 +207,38 @@ def run_real(n=2, m=2, p=2, supg=None, neumann=False, tag=""):
     print("real", n, m, p, tag, "zhat", sys_.zhat, "its", info["iterations"])
 
 
+def make_fem_tables():
+    """Reference-element tables of the device assembly (fem.py) from the
+    reference's fem_basis / assembly helpers."""
+    from mehdg import fem_basis as FB
+    out = {}
+    for m, p in ((1, 1), (2, 2), (3, 2), (2, 3), (1, 4), (2, 5)):
+        for deg in (2 * p + 1, 2 * p + 2):
+            key = f"m{m}p{p}d{deg}"
+            rule = FB.quadrature_rule(2, deg)
+            B = FB.LagrangeBasis(2, p)
+            out[key + "_qp"] = rule.points_ref
+            out[key + "_qw"] = rule.weights
+            out[key + "_val"] = B.eval(rule.points_ref)
+            out[key + "_grad"] = B.grad(rule.points_ref)
+            out[key + "_hess"] = B.hess(rule.points_ref)
+        dm = FB._patch_dof_map(m, p)
+        out[f"m{m}p{p}_cell_map"] = np.array(dm.cell_maps)
+        out[f"m{m}p{p}_edge_nodes"] = dm.edge_nodes
+        mesh = R_mesh.build_structured_macro_mesh(2, 2, m)
+        face = mesh.skeleton[1]
+        side = face.sides()[0]
+        s, w = R_asm._piecewise_quad(R_asm._face_breaks(face, side, m), p + 1)
+        out[f"m{m}p{p}_face_s"] = s
+        out[f"m{m}p{p}_face_w"] = w
+        out[f"m{m}p{p}_trace"] = FB.TraceBasis(m, p).eval(s)
+        g = lambda x: np.cos(2.0 * x[:, 0]) + x[:, 1] ** 2  # noqa: E731
+        dfaces = [f for f in mesh.skeleton if f.tag == "D"][:4]
+        out[f"m{m}p{p}_dface_verts"] = np.stack([f.verts for f in dfaces])
+        out[f"m{m}p{p}_ghat"] = np.stack([R_asm.project_dirichlet(f, g, p) for f in dfaces])
+    np.savez_compressed(HERE / "fem_tables.npz", **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["skeleton", "c1", "real", "c2", "c3"]
     if "skeleton" in which:
@@ -216,6 +248,8 @@ if __name__ == "__main__":
     if "real" in which:
         run_real(2, 2, 2)
         run_real(3, 1, 3)
+    if "fem" in which:
+        make_fem_tables()
     if "asm" in which:  # device-assembly fixtures
         run_real(2, 2, 2, supg="classical-minus", tag="_supg")
         run_real(2, 2, 3, supg="paper-plus", tag="_supgplus")
