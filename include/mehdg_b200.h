@@ -95,8 +95,10 @@ int mh_slab_partition(int64_t n_elem, int64_t elems_per_slab, int nranks, int64_
 
 /* ---- system lifecycle (replaces condense, schur_solver.py:185-254) ---- */
 
-/* Create a system of n_elem macros with Q x Q blocks, nfe = dim+1 slots of
- * width t each (nc = nfe*t), and n_face unknown faces, on device `device`. */
+/* Create a system of n_elem macros with Q x Q blocks, nfe face slots of width
+ * t each (nc = nfe*t; nfe = dim+1 on conforming meshes, up to 6 on 2-D meshes
+ * with hanging faces -- macros with fewer faces leave their last slots empty),
+ * and n_face unknown faces, on device `device`. */
 int mh_create(int device, int nfe, int64_t n_elem, int q, int t, int64_t n_face,
               mh_system** out);
 int mh_destroy(mh_system* sys);
@@ -174,26 +176,31 @@ typedef struct {
   const int32_t* cell_kind; /* ncell: 0 "up", 1 "down" (mesh.py:71-77 order) */
   const int32_t* cell_map;  /* ncell x nb sub-cell dof -> patch dof */
   const int32_t* edge_nodes;/* 3 x t patch dofs along each macro edge */
-  const double* fw;         /* nfq weights of assemble_macro's face rule */
-  const double* th_fwd;     /* nfq x t macro-edge trace basis at t = s */
-  const double* th_rev;     /* nfq x t ... at t = 1 - s */
-  const double* ps;         /* nfq x t face trace basis */
+  const double* fw;         /* 6 x nfq weights of assemble_macro's face rule per side
+                               variant (t0, t1) = (0,1) (1,0) (0,.5) (.5,0) (.5,1) (1,.5),
+                               zero padded */
+  const double* th;         /* 6 x nfq x t macro-edge trace basis at t0 + (t1 - t0) s */
+  const double* ps;         /* 6 x nfq x t face trace basis at s */
   const double* ffw;        /* nffq weights of assemble_face's rule */
   const double* fps;        /* nffq x t */
 } mh_hdg2d_tables;
-/* assemble_macro for N macros: verts[N*3*2], edge_rev[N*3] (1 when the face
- * parameter runs against the macro edge, t0 = 1), edge_dirichlet[N*3] (row of
- * ghat[nD*t] for a Dirichlet face, else -1), fq[N*ncell*nq] (f at the physical
- * quadrature points).  Outputs (device, row-major): A[N*nloc*nloc],
- * B[N*nloc*nc] (op.B), C[N*nc*nloc] (op.C), Ru[N*nloc].  stream: cudaStream_t. */
-int mh_assemble_macros_2d(const mh_hdg2d_tables* tab, int64_t N, const double* verts,
-                          const int8_t* edge_rev, const int32_t* edge_dirichlet,
+/* assemble_macro for N macros with nslot face slots each (3, or up to 6 with
+ * 2:1 hanging faces): verts[N*3*2]; per slot (N*nslot, in the macro's face
+ * order): slot_edge (local edge, -1 = empty slot), slot_var (side variant),
+ * slot_dirichlet (row of ghat[nD*t] for a Dirichlet face, else -1), slot_len
+ * (face length); fq[N*ncell*nq] (f at the physical quadrature points).
+ * Outputs (device, row-major, nc = nslot*t): A[N*nloc*nloc], B[N*nloc*nc]
+ * (op.B), C[N*nc*nloc] (op.C), Ru[N*nloc].  stream: cudaStream_t. */
+int mh_assemble_macros_2d(const mh_hdg2d_tables* tab, int64_t N, int nslot, const double* verts,
+                          const int8_t* slot_edge, const int8_t* slot_var,
+                          const int32_t* slot_dirichlet, const double* slot_len,
                           const double* ghat, const double* fq, double* A, double* B, double* C,
                           double* Ru, void* stream);
 /* assemble_face's D block for F faces: face_sides[F*4] = (left macro, left
- * edge, right macro or -1, right edge); D[F*t*t] row-major. */
+ * edge, right macro or -1, right edge), face_len[F]; D[F*t*t] row-major. */
 int mh_assemble_faces_2d(const mh_hdg2d_tables* tab, int64_t F, const double* verts,
-                         const int32_t* face_sides, double* D, void* stream);
+                         const int32_t* face_sides, const double* face_len, double* D,
+                         void* stream);
 
 /* ---- explicit (matrix-based) Schur, mode "mb" (schur_solver.py:388-420) */
 /* Form S_e = C A^-1 B (nc x nc) per macro on the device; afterwards

@@ -70,8 +70,9 @@ SIGNATURES = {
     "mh_reconstruct": [_p, _dp, _dp],
     "mh_apply_host": [_p, _dp, _dp],
     "mh_apply_host_many": [_p, C.c_int64, _dp, C.c_int64, _dp, C.c_int64],
-    "mh_assemble_macros_2d": [_p, C.c_int64, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p],
-    "mh_assemble_faces_2d": [_p, C.c_int64, _p, _p, _p, _p],
+    "mh_assemble_macros_2d": [_p, C.c_int64, C.c_int, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p,
+                              _p, _p],
+    "mh_assemble_faces_2d": [_p, C.c_int64, _p, _p, _p, _p, _p],
     "mh_precond_host": [_p, _dp, _dp],
     "mh_rhs_host": [_p, _dp],
     "mh_reconstruct_host": [_p, _dp, _dp],

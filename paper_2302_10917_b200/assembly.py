@@ -127,8 +127,7 @@ class _Tables(C.Structure):
                                          "nffq", "supg", "supg_plus")] + \
                [(n, C.c_double) for n in ("kappa", "ax", "ay")] + \
                [(n, C.c_void_p) for n in ("qw", "val", "gref", "href", "cell_kind", "cell_map",
-                                          "edge_nodes", "fw", "th_fwd", "th_rev", "ps", "ffw",
-                                          "fps")]
+                                          "edge_nodes", "fw", "th", "ps", "ffw", "fps")]
 
 
 @dataclass
@@ -151,22 +150,29 @@ class DeviceBlocks:
     tables: dict
 
 
-def _side_orientation(mesh, verts: np.ndarray) -> np.ndarray:
-    """(N, 3) int8: 1 where the face parameter runs against macro edge k
-    (side t0 = 1; mesh.py:228-233 with the canonical lexicographic face vertex
-    order, mesh.py:222-223)."""
-    N = verts.shape[0]
-    rev = np.zeros((N, 3), np.int8)
-    if hasattr(mesh, "vertices_lattice"):  # exact integer lattice order
+def _side_params(mesh, tables: dict) -> np.ndarray:
+    """(F, 2, 2) FaceSide (t0, t1) of every face's left / right side (mesh.py:130-135):
+    for our structured mesh from the exact lattice order of the edge end points
+    (the face vertices are in canonical lexicographic order, mesh.py:222-223);
+    for the reference MacroMesh read from its FaceSide records."""
+    F = len(tables["face_left"])
+    tt = np.zeros((F, 2, 2))
+    if hasattr(mesh, "vertices_lattice"):
         lat = mesh.vertices_lattice[mesh.elem_verts]  # (N, 3, 2)
-        for k, (a, b) in enumerate(fem.EDGE_VERTS):
-            pa, pb = lat[:, a], lat[:, b]
-            rev[:, k] = (pa[:, 0] > pb[:, 0]) | ((pa[:, 0] == pb[:, 0]) & (pa[:, 1] > pb[:, 1]))
-        return rev
-    for face in mesh.skeleton:  # the reference MacroMesh: its FaceSide t0 / t1
-        for side in face.sides():
-            rev[side.macro, side.edge] = 1 if side.t0 > side.t1 else 0
-    return rev
+        for c, fs in enumerate((tables["face_left"], tables["face_right"])):
+            e, k = fs[:, 0], fs[:, 1]
+            ok = e >= 0
+            a = np.array([ev[0] for ev in fem.EDGE_VERTS])[k[ok]]
+            b = np.array([ev[1] for ev in fem.EDGE_VERTS])[k[ok]]
+            pa, pb = lat[e[ok], a], lat[e[ok], b]
+            rev = (pa[:, 0] > pb[:, 0]) | ((pa[:, 0] == pb[:, 0]) & (pa[:, 1] > pb[:, 1]))
+            tt[ok, c, 0] = rev.astype(float)
+            tt[ok, c, 1] = 1.0 - rev
+        return tt
+    for face in mesh.skeleton:
+        for c, side in enumerate(face.sides()):
+            tt[face.id, c] = (side.t0, side.t1)
+    return tt
 
 
 def _face_verts(mesh, fids: np.ndarray) -> np.ndarray:
@@ -210,7 +216,7 @@ def assemble_system_device(mesh, problem: ProblemData, stab: StabilizationConfig
     verts = fem.macro_geometry(mesh)
     N = verts.shape[0]
     Q, t = tab.Q, tab.t
-    nloc, nc = 3 * Q, 3 * t
+    nloc = 3 * Q
 
     def d(x, dtype=torch.float64):
         return torch.as_tensor(np.ascontiguousarray(x), dtype=dtype, device=dev)
@@ -220,29 +226,46 @@ def assemble_system_device(mesh, problem: ProblemData, stab: StabilizationConfig
     fq = np.asarray(problem.f(pts.reshape(-1, 2)), dtype=float).reshape(pts.shape[:3])
     face_tag = np.array([str(tg) for tg in (mesh.face_tag if hasattr(mesh, "face_tag")
                                             else [f.tag for f in mesh.skeleton])])
-    elem_face = np.asarray(tables["elem_face"])
+    elem_face = np.asarray(tables["elem_face"])  # (N, S) faces in slot order, -1 = none
+    S = elem_face.shape[1]
     dfaces = np.nonzero(face_tag == "D")[0]
     drow = np.full(face_tag.size, -1, np.int32)
     drow[dfaces] = np.arange(dfaces.size, dtype=np.int32)
-    edge_dir = drow[elem_face]
+    slot_dir = np.where(elem_face >= 0, drow[np.maximum(elem_face, 0)], -1).astype(np.int32)
     ghat = fem.dirichlet_projection(_face_verts(mesh, dfaces), problem.g_D, p, m) \
         if dfaces.size else np.zeros((1, t))
-    rev = _side_orientation(mesh, verts)
+    # per slot: local edge, side variant (t0, t1) and face length
+    F_all = face_tag.size
+    fverts = _face_verts(mesh, np.arange(F_all))
+    flen = np.linalg.norm(fverts[:, 1] - fverts[:, 0], axis=1)
+    tt = _side_params(mesh, tables)
+    slot_edge = np.full((N, S), -1, np.int8)
+    slot_var = np.zeros((N, S), np.int8)
+    slot_len = np.zeros((N, S))
+    for c, fs in enumerate((np.asarray(tables["face_left"]), np.asarray(tables["face_right"]))):
+        ok = np.nonzero(fs[:, 0] >= 0)[0]
+        e, j = fs[ok, 0], fs[ok, 1]
+        slot_edge[e, j] = np.asarray(tables["face_edge"])[ok, c]
+        slot_var[e, j] = [fem.side_variant(a0, a1) for a0, a1 in tt[ok, c]]
+        slot_len[e, j] = flen[ok]
 
     keep = dict(qw=d(tab.qw), val=d(tab.val), gref=d(tab.gref), href=d(tab.href),
                 cell_kind=d(tab.cell_kind, torch.int32), cell_map=d(tab.cell_map, torch.int32),
-                edge_nodes=d(tab.edge_nodes, torch.int32), fw=d(tab.fw), th_fwd=d(tab.th_fwd),
-                th_rev=d(tab.th_rev), ps=d(tab.ps), ffw=d(tab.ffw), fps=d(tab.fps))
+                edge_nodes=d(tab.edge_nodes, torch.int32), fw=d(tab.fw), th=d(tab.th),
+                ps=d(tab.ps), ffw=d(tab.ffw), fps=d(tab.fps))
     T = _Tables(m=m, p=p, Q=Q, nb=tab.nb, t=t, nq=tab.qw.size, ncell=len(tab.cell_kind),
-                nfq=tab.fw.size, nffq=tab.ffw.size, supg=int(stab.supg),
+                nfq=tab.fw.shape[1], nffq=tab.ffw.size, supg=int(stab.supg),
                 supg_plus=int(stab.supg_variant == "paper-plus"), kappa=float(problem.kappa),
                 ax=float(problem.a[0]), ay=float(problem.a[1]),
                 **{k: v.data_ptr() for k, v in keep.items()})
+    nc = S * t
     A = torch.empty((N, nloc, nloc), dtype=torch.float64, device=dev)
     B = torch.empty((N, nloc, nc), dtype=torch.float64, device=dev)
     Cm = torch.empty((N, nc, nloc), dtype=torch.float64, device=dev)
     Ru = torch.empty((N, nloc), dtype=torch.float64, device=dev)
-    verts_d, rev_d, dir_d = d(verts), d(rev, torch.int8), d(edge_dir, torch.int32)
+    verts_d = d(verts)
+    se_d, sv_d, sd_d, sl_d = (d(slot_edge, torch.int8), d(slot_var, torch.int8),
+                              d(slot_dir, torch.int32), d(slot_len))
     ghat_d, fq_d = d(ghat), d(fq)
     stream = torch.cuda.current_stream(dev).cuda_stream
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -250,19 +273,24 @@ def assemble_system_device(mesh, problem: ProblemData, stab: StabilizationConfig
     ufaces = np.nonzero(uidx >= 0)[0]
     ufaces = ufaces[np.argsort(uidx[ufaces])]
     F = ufaces.size
-    sides = np.concatenate((np.asarray(tables["face_left"])[ufaces],
-                            np.asarray(tables["face_right"])[ufaces]), axis=1).astype(np.int32)
+    fe = np.asarray(tables["face_edge"])[ufaces]
+    sides = np.stack((np.asarray(tables["face_left"])[ufaces, 0], fe[:, 0],
+                      np.asarray(tables["face_right"])[ufaces, 0], fe[:, 1]), axis=1)
+    sides = np.ascontiguousarray(sides, dtype=np.int32)
+    flen_d = d(flen[ufaces])
     D = torch.empty((F, t, t), dtype=torch.float64, device=dev)
     sides_d = d(sides, torch.int32)
     t_host = _time.perf_counter() - t_host0
     ev0.record(torch.cuda.current_stream(dev))
-    check(lib.mh_assemble_macros_2d(C.addressof(T), N, verts_d.data_ptr(), rev_d.data_ptr(),
-                                    dir_d.data_ptr(), ghat_d.data_ptr(), fq_d.data_ptr(),
-                                    A.data_ptr(), B.data_ptr(), Cm.data_ptr(), Ru.data_ptr(),
-                                    stream), "mh_assemble_macros_2d")
+    check(lib.mh_assemble_macros_2d(C.addressof(T), N, S, verts_d.data_ptr(), se_d.data_ptr(),
+                                    sv_d.data_ptr(), sd_d.data_ptr(), sl_d.data_ptr(),
+                                    ghat_d.data_ptr(), fq_d.data_ptr(), A.data_ptr(),
+                                    B.data_ptr(), Cm.data_ptr(), Ru.data_ptr(), stream),
+          "mh_assemble_macros_2d")
     # face blocks in unknown-face order (the order of condense's offsets)
     check(lib.mh_assemble_faces_2d(C.addressof(T), F, verts_d.data_ptr(), sides_d.data_ptr(),
-                                   D.data_ptr(), stream), "mh_assemble_faces_2d")
+                                   flen_d.data_ptr(), D.data_ptr(), stream),
+          "mh_assemble_faces_2d")
     ev1.record(torch.cuda.current_stream(dev))
     Rh = np.zeros((F, t))
     nfaces = np.nonzero(face_tag[ufaces] == "N")[0]

@@ -26,8 +26,11 @@ struct AsmDev {
   mh_hdg2d_tables T;
   int64_t N;
   const double* verts;        // N x 3 x 2
-  const int8_t* edge_rev;     // N x 3: face parameter runs against the edge
-  const int32_t* edge_dir;    // N x 3: row of ghat for a Dirichlet face, else -1
+  int S;                      // face slots per macro (3; up to 6 with hanging faces)
+  const int8_t* slot_edge;    // N x S: local edge of the slot's face, -1 = empty slot
+  const int8_t* slot_var;     // N x S: side variant (fem.SIDE_VARIANTS: t0, t1)
+  const int32_t* slot_dir;    // N x S: row of ghat for a Dirichlet face, else -1
+  const double* slot_len;     // N x S: face length
   const double* ghat;         // nD x t
   const double* fq;           // N x ncell x nq
   double* A;                  // N x nloc x nloc
@@ -86,7 +89,7 @@ __device__ double supg_param(double h, double ax, double ay, double kappa, int p
 // one macro per CTA
 __global__ void __launch_bounds__(kAsmThreads) assemble_macro_kernel(AsmDev a) {
   const mh_hdg2d_tables& T = a.T;
-  const int nb = T.nb, nq = T.nq, Q = T.Q, t = T.t, nloc = 3 * Q, nc = 3 * t, nb2 = nb * nb;
+  const int nb = T.nb, nq = T.nq, Q = T.Q, t = T.t, nloc = 3 * Q, nc = a.S * t, nb2 = nb * nb;
   extern __shared__ double sm[];
   double* tabs = sm;                       // [2 kinds][4: M, Kx, Ky, S][nb*nb]
   double* gph = tabs + 8 * nb2;            // nq x nb x 2
@@ -216,26 +219,31 @@ __global__ void __launch_bounds__(kAsmThreads) assemble_macro_kernel(AsmDev a) {
       }
       __syncthreads();
     }
-    // ---- face terms, slot k = local edge k (assembly.py:252-283)
-    for (int k = 0; k < 3; ++k) {
-      const double n0 = g.nrm[k][0], n1 = g.nrm[k][1];
+    // ---- face terms, one slot per face in the macro's face order (assembly.py:252-283)
+    for (int k = 0; k < a.S; ++k) {
+      const int edge = a.slot_edge[e * a.S + k];
+      if (edge < 0) break;  // no more faces on this macro
+      const double n0 = g.nrm[edge][0], n1 = g.nrm[edge][1];
       const double an = ax * n0 + ay * n1;
       const double tau = fabs(an) + kappa / g.diam;  // stabilization_tau (assembly.py:85-91)
-      const double* TH = a.edge_rev[e * 3 + k] ? T.th_rev : T.th_fwd;
-      const double lenF = g.len[k];
+      const int var = a.slot_var[e * a.S + k];
+      const double* TH = T.th + (int64_t)var * T.nfq * t;
+      const double* PS = T.ps + (int64_t)var * T.nfq * t;
+      const double* FW = T.fw + (int64_t)var * T.nfq;
+      const double lenF = a.slot_len[e * a.S + k];
       for (int ij = threadIdx.x; ij < t * t; ij += blockDim.x) {
         const int i = ij / t, j = ij - i * t;
         double w = 0.0, me = 0.0;
         for (int s = 0; s < T.nfq; ++s) {
-          const double wl = T.fw[s] * lenF;
-          w = fma(TH[s * t + i], wl * T.ps[s * t + j], w);
+          const double wl = FW[s] * lenF;
+          w = fma(TH[s * t + i], wl * PS[s * t + j], w);
           me = fma(TH[s * t + i], wl * TH[s * t + j], me);
         }
         W[ij] = w;
         Me[ij] = me;
       }
       __syncthreads();
-      const int* en = T.edge_nodes + k * t;
+      const int* en = T.edge_nodes + edge * t;
       for (int ij = threadIdx.x; ij < t * t; ij += blockDim.x) {
         const int i = ij / t, j = ij - i * t;
         const int ri = en[i], rj = en[j];
@@ -253,8 +261,8 @@ __global__ void __launch_bounds__(kAsmThreads) assemble_macro_kernel(AsmDev a) {
       __syncthreads();
     }
     // ---- Dirichlet trace elimination R_u -= B[:, slot] ghat (assembly.py:285-290)
-    for (int k = 0; k < 3; ++k) {
-      const int dk = a.edge_dir[e * 3 + k];
+    for (int k = 0; k < a.S; ++k) {
+      const int dk = a.slot_dir[e * a.S + k];
       if (dk < 0) continue;
       const double* gh = a.ghat + (int64_t)dk * t;
       for (int i = threadIdx.x; i < nloc; i += blockDim.x) {
@@ -270,12 +278,13 @@ __global__ void __launch_bounds__(kAsmThreads) assemble_macro_kernel(AsmDev a) {
 // D = (sum over the face's sides of a.n - tau) * Mface (assembly.py:293-312);
 // one warp per unknown face
 __global__ void assemble_face_kernel(mh_hdg2d_tables T, int64_t F, const double* verts,
-                                     const int32_t* sides, double* D) {
+                                     const int32_t* sides, const double* face_len, double* D) {
   const int lane = threadIdx.x & 31;
   const int64_t f = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (f >= F) return;
   const int t = T.t;
-  double coef = 0.0, len = 0.0;
+  double coef = 0.0;
+  const double len = face_len[f];
   for (int sd = 0; sd < 2; ++sd) {
     const int e = sides[f * 4 + 2 * sd], k = sides[f * 4 + 2 * sd + 1];
     if (e < 0) continue;
@@ -284,7 +293,6 @@ __global__ void assemble_face_kernel(mh_hdg2d_tables T, int64_t F, const double*
     const double an = T.ax * g.nrm[k][0] + T.ay * g.nrm[k][1];
     const double tau = fabs(an) + T.kappa / g.diam;
     coef += an - tau;
-    if (sd == 0) len = g.len[k];
   }
   for (int ij = lane; ij < t * t; ij += 32) {
     const int i = ij / t, j = ij - i * t;
@@ -299,16 +307,20 @@ __global__ void assemble_face_kernel(mh_hdg2d_tables T, int64_t F, const double*
 
 using namespace mh;
 
-extern "C" int mh_assemble_macros_2d(const mh_hdg2d_tables* tab, int64_t N, const double* verts,
-                                     const int8_t* edge_rev, const int32_t* edge_dirichlet,
-                                     const double* ghat, const double* fq, double* A, double* B,
-                                     double* C, double* Ru, void* stream) {
-  if (!tab || N < 0 || tab->nb < 1 || tab->nq < 1 || tab->t < 1 || tab->Q < 1) {
+extern "C" int mh_assemble_macros_2d(const mh_hdg2d_tables* tab, int64_t N, int nslot,
+                                     const double* verts, const int8_t* slot_edge,
+                                     const int8_t* slot_var, const int32_t* slot_dirichlet,
+                                     const double* slot_len, const double* ghat,
+                                     const double* fq, double* A, double* B, double* C,
+                                     double* Ru, void* stream) {
+  if (!tab || N < 0 || tab->nb < 1 || tab->nq < 1 || tab->t < 1 || tab->Q < 1 || nslot < 1 ||
+      nslot > kMaxSlots) {
     set_error("mh_assemble_macros_2d: bad arguments");
     return MH_E_ARG;
   }
   if (N == 0) return MH_OK;
-  if (!verts || !edge_rev || !edge_dirichlet || !fq || !A || !B || !C || !Ru) {
+  if (!verts || !slot_edge || !slot_var || !slot_dirichlet || !slot_len || !fq || !A || !B ||
+      !C || !Ru) {
     set_error("mh_assemble_macros_2d: null pointer");
     return MH_E_ARG;
   }
@@ -316,8 +328,11 @@ extern "C" int mh_assemble_macros_2d(const mh_hdg2d_tables* tab, int64_t N, cons
   a.T = *tab;
   a.N = N;
   a.verts = verts;
-  a.edge_rev = edge_rev;
-  a.edge_dir = edge_dirichlet;
+  a.S = nslot;
+  a.slot_edge = slot_edge;
+  a.slot_var = slot_var;
+  a.slot_dir = slot_dirichlet;
+  a.slot_len = slot_len;
   a.ghat = ghat;
   a.fq = fq;
   a.A = A;
@@ -338,19 +353,20 @@ extern "C" int mh_assemble_macros_2d(const mh_hdg2d_tables* tab, int64_t N, cons
 }
 
 extern "C" int mh_assemble_faces_2d(const mh_hdg2d_tables* tab, int64_t F, const double* verts,
-                                    const int32_t* face_sides, double* D, void* stream) {
+                                    const int32_t* face_sides, const double* face_len, double* D,
+                                    void* stream) {
   if (!tab || F < 0 || tab->t < 1) {
     set_error("mh_assemble_faces_2d: bad arguments");
     return MH_E_ARG;
   }
   if (F == 0) return MH_OK;
-  if (!verts || !face_sides || !D) {
+  if (!verts || !face_sides || !face_len || !D) {
     set_error("mh_assemble_faces_2d: null pointer");
     return MH_E_ARG;
   }
   const int wpb = 8;
   assemble_face_kernel<<<(unsigned)((F + wpb - 1) / wpb), wpb * 32, 0, (cudaStream_t)stream>>>(
-      *tab, F, verts, face_sides, D);
+      *tab, F, verts, face_sides, face_len, D);
   MH_CHECK_CUDA(cudaGetLastError());
   return MH_OK;
 }

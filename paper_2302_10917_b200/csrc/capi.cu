@@ -104,7 +104,7 @@ static int need(mh_system* s, bool cond, const char* msg) {
 
 extern "C" int mh_create(int device, int nfe, int64_t n_elem, int q, int t, int64_t n_face,
                          mh_system** out) {
-  if (!out || nfe < 1 || nfe > 4 || n_elem < 0 || q < 1 || t < 1 || n_face < 0) {
+  if (!out || nfe < 1 || nfe > kMaxSlots || n_elem < 0 || q < 1 || t < 1 || n_face < 0) {
     set_error("mh_create: bad sizes");
     return MH_E_ARG;
   }

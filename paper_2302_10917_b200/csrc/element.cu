@@ -208,7 +208,7 @@ element_kernel(ElemArgs a) {
   constexpr int RC = 8;  // gathered slot values per lane (nc <= 256)
   int pr_n[R];
   double dr_n[R];
-  int32_t ef_n[4];
+  int32_t ef_n[kMaxSlots];
   double g_n[RC];
   auto load_meta = [&](int64_t en) {
 #pragma unroll
@@ -218,7 +218,9 @@ element_kernel(ElemArgs a) {
       dr_n[r] = i < Q ? __ldg(a.dinv + en * Q + i) : 0.0;
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) ef_n[k] = k < a.nfe ? __ldg(a.elem_ufac + en * a.nfe + k) : -1;
+#pragma unroll
+    for (int k = 0; k < kMaxSlots; ++k)
+      ef_n[k] = k < a.nfe ? __ldg(a.elem_ufac + en * a.nfe + k) : -1;
   };
   auto gather_next = [&]() {
 #pragma unroll
@@ -229,7 +231,7 @@ element_kernel(ElemArgs a) {
         const int k = c / t, s = c - k * t;
         int f = ef_n[0];
 #pragma unroll
-        for (int kk = 1; kk < 4; ++kk) f = (k == kk) ? ef_n[kk] : f;
+        for (int kk = 1; kk < kMaxSlots; ++kk) f = (k == kk) ? ef_n[kk] : f;
         if (f >= 0)
           v = f < a.F ? __ldg(a.uhat + (int64_t)f * t + s)
                       : __ldg(a.uhalo + (int64_t)(f - a.F) * t + s);

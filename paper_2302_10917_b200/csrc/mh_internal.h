@@ -31,6 +31,9 @@ void set_error(const std::string& msg);
   } while (0)
 
 constexpr int kWarp = 32;
+// face slots per macro: d + 1 on conforming meshes, up to 6 with 2:1 hanging
+// faces in 2-D (two faces per macro edge, mesh.py:264-302)
+constexpr int kMaxSlots = 6;
 constexpr unsigned kFull = 0xffffffffu;
 // fixed reduction partition: results never depend on the device or SM count
 constexpr int kDotBlocks = 512;

@@ -154,6 +154,11 @@ def piecewise_quad(breaks, npts: int):
 JSUB = (np.array([[1.0, 0.0], [0.0, 1.0]]), np.array([[0.0, -1.0], [1.0, 1.0]]))  # up, down
 
 
+# side orientations of a face on a macro edge: (t0, t1) of FaceSide (mesh.py:130-135);
+# the last four are the coarse side of a 2:1 hanging face (mesh.py:264-302)
+SIDE_VARIANTS = ((0.0, 1.0), (1.0, 0.0), (0.0, 0.5), (0.5, 0.0), (0.5, 1.0), (1.0, 0.5))
+
+
 @dataclass
 class AsmTables:
     m: int
@@ -170,39 +175,68 @@ class AsmTables:
     cell_ij: np.ndarray
     cell_map: np.ndarray   # (ncell, nb)
     edge_nodes: np.ndarray  # (3, t)
-    fs: np.ndarray     # (nfq,) macro-side face quadrature parameters
-    fw: np.ndarray     # (nfq,)
-    th_fwd: np.ndarray  # (nfq, t) macro-edge trace basis at t = s
-    th_rev: np.ndarray  # (nfq, t) at t = 1 - s (side with t0 = 1, t1 = 0)
-    ps: np.ndarray     # (nfq, t) face trace basis at s
+    fw: np.ndarray     # (nvar, nfq) assemble_macro's face rule per side variant (zero padded)
+    th: np.ndarray     # (nvar, nfq, t) macro-edge trace basis at t0 + (t1 - t0) s
+    ps: np.ndarray     # (nvar, nfq, t) face trace basis at s
     ffw: np.ndarray    # (nffq,) face-block quadrature (assemble_face)
     fps: np.ndarray    # (nffq, t)
+
+    @property
+    def fs(self):  # conforming forward side: the rule's parameters (tests)
+        return self._fs
+
+    @property
+    def th_fwd(self):
+        return self.th[0, :self._nfq0]
+
+
+def face_rule(m_f: int, m: int, p: int, t0: float, t1: float):
+    """assemble_macro's quadrature on one face side (assembly.py:134-143, 292):
+    breakpoints of the face's trace subdivision united with the macro-edge
+    subdivision mapped to the face parameter, the latter rounded to 12 digits
+    (so for m = 3, 5, ... the set also holds a sliver segment, kept as in the
+    reference)."""
+    breaks = set(np.arange(m_f + 1) / m_f)
+    dt = t1 - t0
+    for c in range(m + 1):
+        sc = (c / m - t0) / dt
+        if 1e-12 < sc < 1 - 1e-12:
+            breaks.add(round(sc, 12))
+    return piecewise_quad(np.array(sorted(breaks)), p + 1)
 
 
 @lru_cache(maxsize=None)
 def asm_tables(m: int, p: int, quad_degree: int) -> AsmTables:
     """Constant tables of assemble_macro / assemble_face (assembly.py:176-322) for a
-    conforming structured mesh (every face is a whole macro edge, m_f = m)."""
+    structured mesh of one subdivision m (m_f = m on every face)."""
     qp, qw = triangle_rule(quad_degree)
     basis = Lagrange(2, p)
     kinds, ij, maps, edge, Q = patch_dof_map(m, p)
-    # assemble_macro's face rule (assembly.py:134-143, 292): breakpoints of the
-    # trace subdivision united with the macro-edge ones rounded to 12 digits
-    # (for m = 3, 5, ... the set holds both c/m and round(c/m, 12), i.e. a
-    # sliver segment; it is kept so the rule is the reference's); the same set
-    # for either side orientation
-    breaks = set(np.arange(m + 1) / m)
-    for c in range(m + 1):
-        sc = c / m
-        if 1e-12 < sc < 1 - 1e-12:
-            breaks.add(round(sc, 12))
-    fs, fw = piecewise_quad(np.array(sorted(breaks)), p + 1)
+    t = m * p + 1
+    rules = [face_rule(m, m, p, t0, t1) for t0, t1 in SIDE_VARIANTS]
+    nfq = max(s.size for s, _ in rules)
+    fw = np.zeros((len(rules), nfq))
+    th = np.zeros((len(rules), nfq, t))
+    ps = np.zeros((len(rules), nfq, t))
+    for v, ((s, w), (t0, t1)) in enumerate(zip(rules, SIDE_VARIANTS)):
+        fw[v, :s.size] = w
+        th[v, :s.size] = trace_eval(m, p, t0 + (t1 - t0) * s)
+        ps[v, :s.size] = trace_eval(m, p, s)
     ffs, ffw = piecewise_quad(np.arange(m + 1) / m, p + 1)  # assemble_face (assembly.py:302)
-    return AsmTables(m=m, p=p, Q=Q, nb=basis.n, t=m * p + 1, qp=qp, qw=qw,
-                     val=basis.eval(qp), gref=basis.grad(qp), href=basis.hess(qp),
-                     cell_kind=kinds, cell_ij=ij, cell_map=maps, edge_nodes=edge,
-                     fs=fs, fw=fw, th_fwd=trace_eval(m, p, fs), th_rev=trace_eval(m, p, 1.0 - fs),
-                     ps=trace_eval(m, p, fs), ffw=ffw, fps=trace_eval(m, p, ffs))
+    tab = AsmTables(m=m, p=p, Q=Q, nb=basis.n, t=t, qp=qp, qw=qw,
+                    val=basis.eval(qp), gref=basis.grad(qp), href=basis.hess(qp),
+                    cell_kind=kinds, cell_ij=ij, cell_map=maps, edge_nodes=edge,
+                    fw=fw, th=th, ps=ps, ffw=ffw, fps=trace_eval(m, p, ffs))
+    tab._fs, tab._nfq0 = rules[0][0], rules[0][0].size
+    return tab
+
+
+def side_variant(t0: float, t1: float) -> int:
+    for v, (a, b) in enumerate(SIDE_VARIANTS):
+        if abs(t0 - a) < 1e-12 and abs(t1 - b) < 1e-12:
+            return v
+    raise NotImplementedError(f"face side parameters ({t0}, {t1}) are not a conforming or "
+                              "2:1 hanging configuration")
 
 
 def macro_geometry(mesh) -> np.ndarray:

@@ -165,29 +165,49 @@ def mesh_tables(mesh) -> dict:
     if isinstance(mesh, StructuredMacroMesh):
         return dict(nfe=mesh.d + 1, n_elem=mesh.n_elem, face_unknown=mesh.face_unknown,
                     elem_face=mesh.elem_face, face_left=mesh.face_left,
-                    face_right=mesh.face_right)
+                    face_right=mesh.face_right,
+                    face_edge=np.stack((mesh.face_left[:, 1], mesh.face_right[:, 1]), axis=1),
+                    hanging=False)
     skel = list(mesh.skeleton)
-    n_elem = len(mesh.macro_elements)
+    macros = list(mesh.macro_elements)
+    n_elem = len(macros)
     nfe = getattr(mesh, "d", 2) + 1
     F = len(skel)
     face_left = np.full((F, 2), -1, np.int32)
     face_right = np.full((F, 2), -1, np.int32)
+    face_edge = np.full((F, 2), -1, np.int32)
     face_unknown = np.zeros(F, np.int8)
-    elem_face = np.full((n_elem, nfe), -1, np.int32)
+    # 2:1 hanging faces (mesh.py:264-302): a macro edge carries two faces; the
+    # macro's slots are then its face lists in order, edge by edge
+    # (assemble_macro's face_slots, assembly.py:241-249), up to 6 in 2-D
+    hanging = all(hasattr(e, "faces") for e in macros) and \
+        any(len(fl) > 1 for e in macros for fl in e.faces)
+    if hanging:
+        slots = [[int(fid) for k in range(nfe) for fid in e.faces[k]] for e in macros]
+        nfe = max(len(sl) for sl in slots)
+        elem_face = np.full((n_elem, nfe), -1, np.int32)
+        slot_of = {}
+        for e, sl in enumerate(slots):
+            elem_face[e, :len(sl)] = sl
+            for j, fid in enumerate(sl):
+                slot_of[(e, fid)] = j
+    else:
+        elem_face = np.full((n_elem, nfe), -1, np.int32)
     for pos, face in enumerate(skel):
         if face.id != pos:
             raise ValueError("skeleton face ids must be 0..F-1 in order")
-        sides = face.sides()
-        for col, side in enumerate(sides):
-            (face_left if col == 0 else face_right)[pos] = (side.macro, side.edge)
-            if elem_face[side.macro, side.edge] != -1:
-                raise NotImplementedError(
-                    "more than one face per macro edge (hanging faces) is not on the "
-                    "B200 path yet (SURVEY.md 8(f) row 4)")
-            elem_face[side.macro, side.edge] = pos
+        for col, side in enumerate(face.sides()):
+            slot = slot_of[(side.macro, pos)] if hanging else side.edge
+            (face_left if col == 0 else face_right)[pos] = (side.macro, slot)
+            face_edge[pos, col] = side.edge
+            if not hanging:
+                if elem_face[side.macro, side.edge] != -1:
+                    raise ValueError("two faces on one macro edge without face lists")
+                elem_face[side.macro, side.edge] = pos
         face_unknown[pos] = 0 if face.tag == "D" else 1
     return dict(nfe=nfe, n_elem=n_elem, face_unknown=face_unknown, elem_face=elem_face,
-                face_left=face_left, face_right=face_right)
+                face_left=face_left, face_right=face_right, face_edge=face_edge,
+                hanging=hanging)
 
 
 def condense_tables(tables: dict) -> dict:

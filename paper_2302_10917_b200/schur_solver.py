@@ -221,34 +221,37 @@ class CondensedSystem:
 
 def _stack_ops(local_ops: list, face_ops: dict, tables: dict):
     """Stack LocalOperators / FaceOperator blocks into the C-ABI layouts,
-    checking the uniform-slot layout of assemble_macro (assembly.py:241-249)."""
+    checking the slot layout of assemble_macro (assembly.py:241-249): slot k of a
+    macro owns columns [k t, (k+1) t); macros with fewer faces than the widest
+    one (2:1 hanging faces) are padded with empty slots."""
     N = len(local_ops)
     op0 = local_ops[0]
     nloc = int(op0.R_u.size)
-    nc = int(op0.B.shape[1])
     nfe = tables["nfe"]
-    if nc % nfe:
-        raise NotImplementedError("non-uniform face slots are not on the B200 path")
-    t = nc // nfe
+    sl0 = op0.face_slots[0][1]
+    t = int(sl0.stop - sl0.start)
+    nc = nfe * t
     A = np.empty((N, nloc, nloc))
-    B = np.empty((N, nloc, nc))
-    Cm = np.empty((N, nc, nloc))
+    B = np.zeros((N, nloc, nc))
+    Cm = np.zeros((N, nc, nloc))
     Ru = np.empty((N, nloc))
     c_is_bt = True
     for e, op in enumerate(local_ops):
         if op.macro_id != e:
             raise ValueError("local_ops must be ordered by macro id")
         a = op.A.toarray() if hasattr(op.A, "toarray") else np.asarray(op.A)
-        if a.shape != (nloc, nloc) or op.B.shape != (nloc, nc) or op.C.shape != (nc, nloc):
-            raise NotImplementedError("all macros must share one block shape on the B200 path")
+        nce = len(op.face_slots) * t
+        if a.shape != (nloc, nloc) or op.B.shape != (nloc, nce) or op.C.shape != (nce, nloc) \
+                or nce > nc:
+            raise NotImplementedError("all macros must share one block size and slot width")
         for k, (fid, sl) in enumerate(op.face_slots):
             if sl.start != k * t or sl.stop != (k + 1) * t:
                 raise NotImplementedError("face slot k must own columns [k t, (k+1) t)")
             if tables["elem_face"][e, k] != fid:
                 raise ValueError("face_slots disagree with the mesh skeleton")
         A[e] = a
-        B[e] = op.B
-        Cm[e] = op.C
+        B[e, :, :nce] = op.B
+        Cm[e, :nce] = op.C
         Ru[e] = op.R_u
         if c_is_bt and not np.array_equal(op.C, op.B.T):
             c_is_bt = False

@@ -207,6 +207,74 @@ def run_real(n=2, m=2, p=2, supg=None, neumann=False, tag=""):
     print("real", n, m, p, tag, "zhat", sys_.zhat, "its", info["iterations"])
 
 
+def mesh_arrays(M):
+    """Plain-array description of a reference MacroMesh (incl. hanging faces) from
+    which the tests rebuild a duck-typed mesh without importing the reference."""
+    N, F = len(M.macro_elements), len(M.skeleton)
+    faces = np.full((N, 6), -1, np.int64)
+    for e in M.macro_elements:
+        flat = [fid for k in range(3) for fid in e.faces[k]]
+        faces[e.id, :len(flat)] = flat
+    side = np.full((F, 2, 4), -1.0)
+    for f in M.skeleton:
+        for c, sd in enumerate(f.sides()):
+            side[f.id, c] = (sd.macro, sd.edge, sd.t0, sd.t1)
+    return dict(mesh_verts=np.stack([e.verts for e in M.macro_elements]),
+                mesh_level=np.array([e.level for e in M.macro_elements]),
+                mesh_m=np.array([e.m for e in M.macro_elements]),
+                mesh_faces=faces,
+                face_verts=np.stack([f.verts for f in M.skeleton]),
+                face_side=side,
+                face_tag=np.array([f.tag for f in M.skeleton]),
+                face_mf=np.array([f.m_f for f in M.skeleton]),
+                face_hanging=np.array([f.hanging for f in M.skeleton]))
+
+
+def run_adaptive(n=2, m=2, p=2, marks=({0},), tag=""):
+    """Reference blocks and results on a 2:1 refined mesh with hanging faces
+    (mesh.py:428-463)."""
+    case = make_benchmark("tanh", 0.4, (1.0, 1.0))
+    M = R_mesh.build_structured_macro_mesh(2, n, m)
+    for mk in marks:
+        M = R_mesh.refine_macros(M, set(mk))
+    pool = R.WorkerPool(1)
+    stab = R_asm.StabilizationConfig()
+    local_ops, face_ops = R.assemble_system(M, case.problem(), stab, p, pool)
+    cfg = R.SolverConfig(tol=1e-12)
+    sys_ = R.condense(M, local_ops, face_ops, cfg, pool=pool)
+    rng = np.random.default_rng(3)
+    xs = rng.standard_normal((3, sys_.zhat))
+    nc_max = max(o.B.shape[1] for o in local_ops)
+    nloc = local_ops[0].R_u.size
+
+    def pad(b, axis):
+        out = np.zeros((nloc, nc_max) if axis == 1 else (nc_max, nloc))
+        if axis == 1:
+            out[:, :b.shape[1]] = b
+        else:
+            out[:b.shape[0]] = b
+        return out
+
+    out = mesh_arrays(M)
+    out.update(
+        A=np.stack([np.asarray(o.A.toarray() if hasattr(o.A, "toarray") else o.A)
+                    for o in local_ops]),
+        B=np.stack([pad(o.B, 1) for o in local_ops]), C=np.stack([pad(o.C, 0) for o in local_ops]),
+        nslot=np.array([len(o.face_slots) for o in local_ops]),
+        R_u=np.stack([o.R_u for o in local_ops]),
+        D=np.stack([face_ops[f].D for f in sorted(face_ops)]),
+        R_hat=np.stack([face_ops[f].R_hat for f in sorted(face_ops)]),
+        face_ids=np.array(sorted(face_ops)), f=sys_.f_vec, xs=xs,
+        w=np.stack([R.apply_schur(sys_, v) for v in xs]),
+        z=np.stack([R.apply_preconditioner(sys_, v) for v in xs]), n=n, m=m, p=p)
+    x, info = R.gmres(lambda v: R.apply_schur(sys_, v), sys_.f_vec, cfg,
+                      precond=lambda v: R.apply_preconditioner(sys_, v))
+    out.update(x=x, iterations=info["iterations"], U=np.stack(R.reconstruct_interior(sys_, x)))
+    np.savez_compressed(HERE / f"adaptive_tanh_n{n}m{m}p{p}{tag}.npz", **out)
+    print("adaptive", n, m, p, tag, "N", len(local_ops), "hanging",
+          int(sum(f.hanging for f in M.skeleton)), "zhat", sys_.zhat, "its", info["iterations"])
+
+
 def make_fem_tables():
     """Reference-element tables of the device assembly (fem.py) from the
     reference's fem_basis / assembly helpers."""
@@ -250,6 +318,9 @@ if __name__ == "__main__":
         run_real(3, 1, 3)
     if "fem" in which:
         make_fem_tables()
+    if "adaptive" in which:  # hanging faces
+        run_adaptive(2, 2, 2, marks=({0},))
+        run_adaptive(2, 1, 3, marks=({0, 5}, {1}), tag="_2lev")
     if "asm" in which:  # device-assembly fixtures
         run_real(2, 2, 2, supg="classical-minus", tag="_supg")
         run_real(2, 2, 3, supg="paper-plus", tag="_supgplus")
