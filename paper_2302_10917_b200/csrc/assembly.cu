@@ -20,7 +20,7 @@
 namespace mh {
 namespace {
 
-constexpr int kAsmThreads = 256;
+constexpr int kAsmThreads = 128;
 
 struct AsmDev {
   mh_hdg2d_tables T;
@@ -346,7 +346,7 @@ extern "C" int mh_assemble_macros_2d(const mh_hdg2d_tables* tab, int64_t N, int 
   int dev = 0, sms = 0;
   MH_CHECK_CUDA(cudaGetDevice(&dev));
   MH_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const int64_t grid = std::min<int64_t>(N, (int64_t)sms * 8);
+  const int64_t grid = std::min<int64_t>(N, (int64_t)sms * 16);
   assemble_macro_kernel<<<(unsigned)grid, kAsmThreads, smem, (cudaStream_t)stream>>>(a);
   MH_CHECK_CUDA(cudaGetLastError());
   return MH_OK;
