@@ -18,4 +18,9 @@ ncu --set full --import-source on --clock-control none -k regex:lu_tile -c 1 \
   -o $out/lu_c2 python tools/lu_probe.py c2 1 > $out/ncu_lu.log 2>&1
 ncu --set full --import-source on --clock-control none -k element_kernel -s 1 -c 1 \
   -o $out/element_c3 python bench.py --config c3 --steps 3 --warmup 3 --no-cpu-baseline --no-mb --no-asm > $out/ncu_el3.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:assemble_macro -c 1 \
+  -o $out/assembly python tools/asm_probe.py 128 2 3 1 > $out/ncu_asm.log 2>&1
+python tools/asm_probe.py 128 2 3 3 > $out/asm_probe.txt 2>&1
+for c in c2 c3 c5n20; do python tools/lu_probe.py $c 4 >> $out/lu_probe.txt 2>&1; done
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/fp64_peak tools/fp64_peak.cu && ./tools/fp64_peak > $out/fp64_peak.txt 2>&1
 ls -la $out
