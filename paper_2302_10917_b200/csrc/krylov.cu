@@ -13,6 +13,7 @@
 // as the reference does them in numpy.
 
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "mh_internal.h"
@@ -25,8 +26,20 @@ struct Krylov {
   DBuf<double> V, w, tmp, tmp2, part, hcol, ydev, scal;
   DBuf<unsigned> ticket;
   double* h_host = nullptr;  // pinned
+  bool persistent = false;   // a system's workspace, reused across solves
+  // CUDA graphs of the Arnoldi step's MGS block, one per basis size k (captured
+  // on first use, replayed afterwards; they bake in the buffer addresses above)
+  std::vector<cudaGraphExec_t> mgs;
+  cudaStream_t gs = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  void drop_graphs() {
+    for (cudaGraphExec_t& g : mgs)
+      if (g) cudaGraphExecDestroy(g);
+    mgs.clear();
+  }
   int alloc(int64_t n_, int restart_) {
     if (n_ == n && restart_ == restart && V.p) return MH_OK;
+    drop_graphs();
     n = n_;
     restart = restart_;
     MH_CHECK(V.alloc((size_t)(restart + 1) * (size_t)n));
@@ -44,6 +57,10 @@ struct Krylov {
     return MH_OK;
   }
   ~Krylov() {
+    drop_graphs();
+    if (gs) cudaStreamDestroy(gs);
+    if (ev_in) cudaEventDestroy(ev_in);
+    if (ev_out) cudaEventDestroy(ev_out);
     V.release(); w.release(); tmp.release(); tmp2.release(); part.release();
     hcol.release(); ydev.release(); scal.release(); ticket.release();
     if (h_host) cudaFreeHost(h_host);
@@ -193,6 +210,56 @@ int gmres_core(cudaStream_t st, Krylov* K, int64_t n, const OpFn& A, const OpFn&
                double* x, int* iterations, int* converged, double* hist_host, int hist_cap,
                int* hist_len);
 
+// The MGS block of Arnoldi step k: H[0..k, k] and H[k+1, k] = ||w||, V[k+1] = w / H[k+1, k],
+// and the new Hessenberg column copied to the pinned host buffer.
+int enqueue_mgs(cudaStream_t st, Krylov* K, int64_t n, int k) {
+  double* V = K->V.p;
+  for (int i = 0; i <= k; ++i) {
+    const double* Vi = V + (size_t)i * n;
+    const double* Vp = i > 0 ? V + (size_t)(i - 1) * n : nullptr;
+    const double* coef = i > 0 ? K->hcol.p + (i - 1) : nullptr;
+    MH_CHECK(dot_dev(st, K, n, K->w.p, Vp, coef, Vi, 1, K->hcol.p + i));
+  }
+  MH_CHECK(dot_dev(st, K, n, K->w.p, V + (size_t)k * n, K->hcol.p + k, nullptr, 2,
+                   K->hcol.p + k + 1));
+  normalize_kernel<<<dim3(1184), dim3(256), 0, st>>>(n, K->w.p, K->hcol.p + k + 1,
+                                                     V + (size_t)(k + 1) * n);
+  MH_CHECK_CUDA(cudaGetLastError());
+  MH_CHECK_CUDA(cudaMemcpyAsync(K->h_host, K->hcol.p, sizeof(double) * (k + 2),
+                                cudaMemcpyDeviceToHost, st));
+  return MH_OK;
+}
+
+// Replays (capturing on first use) the graph of step k on a private stream
+// ordered after `st`; returns with the Hessenberg column in K->h_host.  The
+// k + 3 launches of a step then cost one graph launch: same kernels, same
+// arguments, bitwise the same results.
+int run_mgs(cudaStream_t st, Krylov* K, int64_t n, int k) {
+  if (!K->gs) {
+    MH_CHECK_CUDA(cudaStreamCreateWithFlags(&K->gs, cudaStreamNonBlocking));
+    MH_CHECK_CUDA(cudaEventCreateWithFlags(&K->ev_in, cudaEventDisableTiming));
+    MH_CHECK_CUDA(cudaEventCreateWithFlags(&K->ev_out, cudaEventDisableTiming));
+  }
+  if ((int)K->mgs.size() < K->restart) K->mgs.resize((size_t)K->restart, nullptr);
+  if (!K->mgs[k]) {
+    cudaGraph_t g = nullptr;
+    MH_CHECK_CUDA(cudaStreamBeginCapture(K->gs, cudaStreamCaptureModeThreadLocal));
+    const int st_enq = enqueue_mgs(K->gs, K, n, k);
+    const cudaError_t ce = cudaStreamEndCapture(K->gs, &g);
+    MH_CHECK(st_enq);
+    MH_CHECK_CUDA(ce);
+    MH_CHECK_CUDA(cudaGraphInstantiate(&K->mgs[k], g, 0));
+    cudaGraphDestroy(g);
+  }
+  MH_CHECK_CUDA(cudaEventRecord(K->ev_in, st));
+  MH_CHECK_CUDA(cudaStreamWaitEvent(K->gs, K->ev_in, 0));
+  MH_CHECK_CUDA(cudaGraphLaunch(K->mgs[k], K->gs));
+  MH_CHECK_CUDA(cudaEventRecord(K->ev_out, K->gs));
+  MH_CHECK_CUDA(cudaStreamWaitEvent(st, K->ev_out, 0));
+  MH_CHECK_CUDA(cudaEventSynchronize(K->ev_out));
+  return MH_OK;
+}
+
 struct CommScope {  // binds the communicator of a system to the dot products
   explicit CommScope(mh_system* s) { g_comm_sys = s; }
   ~CommScope() { g_comm_sys = nullptr; }
@@ -229,6 +296,9 @@ int gmres_core(cudaStream_t st, Krylov* K, int64_t n, const OpFn& A, const OpFn&
     return MH_OK;
   }
   const int m = restart;
+  const char* gv = getenv("MEHDG_GMRES_GRAPHS");
+  const bool use_graphs = K->persistent && !(g_comm_sys && g_comm_sys->nranks > 1) &&
+                          !(gv && gv[0] == '0');
   std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), y(m);
   auto Hat = [&](int i, int k) -> double& { return H[(size_t)i * m + k]; };
   double* V = K->V.p;
@@ -263,18 +333,14 @@ int gmres_core(cudaStream_t st, Krylov* K, int64_t n, const OpFn& A, const OpFn&
     for (int k = 0; k < m; ++k) {
       double* Vk = V + (size_t)k * n;
       MH_CHECK(apply_MA(A, M, MA, Vk, K->w.p, K->tmp.p));
-      // MGS: H[i,k] = V[i].w ; w -= H[i,k] V[i]   (fused one step behind)
-      for (int i = 0; i <= k; ++i) {
-        const double* Vi = V + (size_t)i * n;
-        const double* Vp = i > 0 ? V + (size_t)(i - 1) * n : nullptr;
-        const double* coef = i > 0 ? K->hcol.p + (i - 1) : nullptr;
-        MH_CHECK(dot_dev(st, K, n, K->w.p, Vp, coef, Vi, 1, K->hcol.p + i));
+      // MGS: H[i,k] = V[i].w ; w -= H[i,k] V[i]   (fused one step behind), as one
+      // CUDA graph per k on a single device (the multi-rank dots go through NCCL)
+      if (use_graphs) {
+        MH_CHECK(run_mgs(st, K, n, k));
+      } else {
+        MH_CHECK(enqueue_mgs(st, K, n, k));
+        MH_CHECK_CUDA(cudaStreamSynchronize(st));
       }
-      MH_CHECK(dot_dev(st, K, n, K->w.p, V + (size_t)k * n, K->hcol.p + k, nullptr, 2,
-                       K->hcol.p + k + 1));
-      normalize_kernel<<<vg, vb, 0, st>>>(n, K->w.p, K->hcol.p + k + 1, V + (size_t)(k + 1) * n);
-      MH_CHECK_CUDA(cudaGetLastError());
-      MH_CHECK(read_scalars(st, K, K->hcol.p, k + 2));
       for (int i = 0; i <= k + 1; ++i) Hat(i, k) = K->h_host[i];
       if (!(Hat(k + 1, k) > 1e-300)) breakdown = true;
       for (int i = 0; i < k; ++i) {
@@ -402,7 +468,10 @@ extern "C" int mh_gmres(mh_system* s, double tol, int restart, int maxiter, int 
     return MH_E_STATE;
   }
   MH_CHECK_CUDA(cudaSetDevice(s->device));
-  if (!s->kry) s->kry = new Krylov();
+  if (!s->kry) {
+    s->kry = new Krylov();
+    s->kry->persistent = true;
+  }
   const int64_t n = s->F * (int64_t)s->t;
   MH_CHECK(s->kry->alloc(n, restart));
   OpFn A, M, MA;
