@@ -246,7 +246,7 @@ def assemble_system_device(mesh, problem: ProblemData, stab: StabilizationConfig
         ok = np.nonzero(fs[:, 0] >= 0)[0]
         e, j = fs[ok, 0], fs[ok, 1]
         slot_edge[e, j] = np.asarray(tables["face_edge"])[ok, c]
-        slot_var[e, j] = [fem.side_variant(a0, a1) for a0, a1 in tt[ok, c]]
+        slot_var[e, j] = fem.side_variant(tt[ok, c, 0], tt[ok, c, 1])
         slot_len[e, j] = flen[ok]
 
     keep = dict(qw=d(tab.qw), val=d(tab.val), gref=d(tab.gref), href=d(tab.href),

@@ -231,12 +231,16 @@ def asm_tables(m: int, p: int, quad_degree: int) -> AsmTables:
     return tab
 
 
-def side_variant(t0: float, t1: float) -> int:
+def side_variant(t0, t1):
+    """Index into SIDE_VARIANTS of FaceSide parameters (t0, t1); arrays accepted."""
+    t0, t1 = np.asarray(t0, float), np.asarray(t1, float)
+    out = np.full(t0.shape, -1, np.int64)
     for v, (a, b) in enumerate(SIDE_VARIANTS):
-        if abs(t0 - a) < 1e-12 and abs(t1 - b) < 1e-12:
-            return v
-    raise NotImplementedError(f"face side parameters ({t0}, {t1}) are not a conforming or "
-                              "2:1 hanging configuration")
+        out[(np.abs(t0 - a) < 1e-12) & (np.abs(t1 - b) < 1e-12)] = v
+    if (out < 0).any():
+        raise NotImplementedError("face side parameters are not a conforming or 2:1 hanging "
+                                  "configuration")
+    return int(out) if out.ndim == 0 else out
 
 
 def macro_geometry(mesh) -> np.ndarray:
@@ -257,7 +261,7 @@ def quad_points(verts: np.ndarray, tab: AsmTables) -> np.ndarray:
         v0ref = np.array([i * h, j * h]) if kind == 0 else np.array([(i + 1) * h, j * h])
         Jc = J @ (JSUB[kind] / m)
         v0 = verts[:, 0] + J @ v0ref
-        out[:, c] = np.einsum("qk,nlk->nql", tab.qp, Jc) + v0[:, None, :]
+        out[:, c] = np.swapaxes(Jc @ tab.qp.T, 1, 2) + v0[:, None, :]
     return out
 
 
