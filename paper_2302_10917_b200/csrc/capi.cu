@@ -123,9 +123,6 @@ extern "C" int mh_create(int device, int nfe, int64_t n_elem, int q, int t, int6
   s->nc = nfe * t;
   s->F = n_face;
   cudaDeviceGetAttribute(&s->max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-  if (const char* v = getenv("MEHDG_L2_PERSIST")) {  // tuning experiment: L2 set-aside bytes
-    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)atoll(v));
-  }
   cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, device);
   cudaError_t e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
   if (e != cudaSuccess) {
