@@ -62,26 +62,46 @@ class SolverConfig:
 
 
 class WorkerPool:
-    """API stand-in for schur_solver.py:59-102.  On the device every macro and
-    face is its own warp, so there is nothing to partition on the host; the
-    pool keeps ``workers``/``busy``/``lbf``/``map`` for callers that use them."""
+    """schur_solver.py:59-102: a fixed round-robin partition of independent host
+    tasks onto threads (item i runs on worker i mod W, so results never depend on
+    the worker count), with per-worker thread CPU time for the load-balance
+    factor.  On the B200 path the macros and faces are device warps; the pool
+    serves host-side callers (e.g. a reference ``assemble_system`` fed to
+    ``solve(..., assemble=...)``) and the report's ``lbf`` / ``worker_busy``."""
 
     def __init__(self, workers: int = 1):
+        from concurrent.futures import ThreadPoolExecutor
+
         self.workers = max(1, int(workers))
         self.busy = np.zeros(self.workers)
+        self._ex = ThreadPoolExecutor(max_workers=self.workers) if self.workers > 1 else None
 
     def map(self, fn: Callable, items) -> list:
-        t0 = time.thread_time()
-        out = [fn(x) for x in items]
-        self.busy[0] += time.thread_time() - t0
+        items = list(items)
+        out = [None] * len(items)
+
+        def chunk(w):
+            t0 = time.thread_time()
+            for i in range(w, len(items), self.workers):
+                out[i] = fn(items[i])
+            self.busy[w] += time.thread_time() - t0
+
+        if self._ex is None:
+            chunk(0)
+        else:
+            for f in [self._ex.submit(chunk, w) for w in range(self.workers)]:
+                f.result()
         return out
 
     @property
     def lbf(self) -> float:
-        return 1.0
+        mx = float(self.busy.max(initial=0.0))
+        return 1.0 if mx == 0.0 else float(self.busy.mean()) / mx
 
     def close(self):
-        pass
+        if self._ex is not None:
+            self._ex.shutdown(wait=True)
+            self._ex = None
 
 
 def _torch():

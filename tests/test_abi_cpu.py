@@ -156,3 +156,36 @@ def test_report_csv_round_trip(tmp_path):
     back = P.read_csv(str(path))
     assert back == rows
     assert P.rows_to_csv(rows, cols).splitlines()[1].split(",")[5] == "0.30000000000000004"
+
+
+def test_solver_config_validation():
+    import paper_2302_10917_b200 as P
+
+    for bad in (dict(tol=0.0), dict(tol=1.0), dict(preconditioner="ilu"), dict(mode="x")):
+        with pytest.raises(ValueError):
+            P.SolverConfig(**bad)
+    cfg = P.SolverConfig()
+    assert (cfg.tol, cfg.restart, cfg.maxiter, cfg.preconditioner, cfg.mode) == \
+        (1e-6, 100, 10000, "dinv", "mf")
+
+
+def test_worker_pool_static_partition():
+    """schur_solver.py:59-102: round-robin items, results independent of workers."""
+    import paper_2302_10917_b200 as P
+
+    items = list(range(37))
+    ref = [x * x + 1 for x in items]
+    for w in (1, 2, 8):
+        pool = P.WorkerPool(w)
+        seen = []
+        assert pool.map(lambda x: (seen.append(x), x * x + 1)[1], items) == ref
+        assert sorted(seen) == items and pool.busy.shape == (w,)
+        assert 0.0 < pool.lbf <= 1.0
+        pool.close()
+
+
+def test_singular_exceptions_carry_ids():
+    import paper_2302_10917_b200 as P
+
+    assert P.SingularLocalBlock(7).args[0] == 7
+    assert P.SingularFaceBlock(3).args[0] == 3
