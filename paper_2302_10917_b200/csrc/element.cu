@@ -409,13 +409,8 @@ size_t smem_bytes(int nc) {
          (size_t)kWPB * ((nc + 3) & ~3) * sizeof(double);
 }
 
-template <int R, int MODE>
-int launch_rm(mh_system* s, const ElemArgs& a) {
-  // 16 KB rings of four 4 KB chunks, 3 CTAs = 12 consumer warps per SM.
-  // Measured alternatives at c2: 8 KB rings of 2 KB chunks at 4 CTAs/SM
-  // -13%, 12 KB rings of three 4 KB chunks at 4 CTAs/SM -1.5%.
-  constexpr int RING = 2048;
-  constexpr int CH = 512;
+template <int R, int MODE, int RING, int CH>
+int launch_rc(mh_system* s, const ElemArgs& a) {
   static_assert(kStreamChunk % CH == 0, "HBM padding must be a multiple of the ring chunk");
   const size_t smem = smem_bytes<RING, CH>(s->nc);
   auto kern = element_kernel<R, MODE, RING, CH>;
@@ -430,6 +425,18 @@ int launch_rm(mh_system* s, const ElemArgs& a) {
   kern<<<(unsigned)grid, kThreads, smem, s->stream>>>(a);
   MH_CHECK_CUDA(cudaGetLastError());
   return MH_OK;
+}
+
+template <int R, int MODE>
+int launch_rm(mh_system* s, const ElemArgs& a) {
+  // 16 KB rings of four 4 KB chunks, 3 CTAs = 12 consumer warps per SM.
+  // Measured alternatives at c2: 8 KB rings of 2 KB chunks at 4 CTAs/SM
+  // -13%, 12 KB rings of three 4 KB chunks at 4 CTAs/SM -1.5%.
+  const char* cv = getenv("MEHDG_ELEM_CH");
+  const int ch = cv ? atoi(cv) : 512;
+  if (ch == 256) return launch_rc<R, MODE, 2048, 256>(s, a);
+  if (ch == 128) return launch_rc<R, MODE, 2048, 128>(s, a);
+  return launch_rc<R, MODE, 2048, 512>(s, a);
 }
 
 template <int MODE>

@@ -108,7 +108,9 @@ struct Pipe {
   static constexpr int S = RING / CH;
   static_assert(RING % CH == 0 && S >= 2, "ring must hold >= 2 chunks");
 
-  // producer warp, lane 0: feed the NCONS consumer streams until done
+  // producer warp, lane 0: feed the NCONS consumer streams until done.  The
+  // per-chunk path is a pointer bump: the segment table (shared memory) is
+  // only consulted when a consumer's stream crosses into its next segment.
   static __device__ void produce(double* rings, uint64_t* full, uint64_t* empty,
                                  const Segment* seg, int nseg, int64_t warp0, int64_t W,
                                  int64_t nmacro, int ncons) {
@@ -116,11 +118,14 @@ struct Pipe {
     const uint64_t pol_last = l2_policy_evict_last();
     int per = 0;
     for (int s = 0; s < nseg; ++s) per += seg[s].nch;
-    int64_t pe[NCONS];
-    uint32_t issued[NCONS], nchunks[NCONS];
-    int ps[NCONS], pq[NCONS];
     int first_seg = 0;
     while (first_seg < nseg && seg[first_seg].nch == 0) ++first_seg;
+    const double* src[NCONS];
+    uint64_t pol[NCONS];
+    int64_t pe[NCONS];
+    uint32_t issued[NCONS], nchunks[NCONS];
+    int ps[NCONS], rem[NCONS];
+#pragma unroll
     for (int w = 0; w < NCONS; ++w) {
       const int64_t e0 = warp0 + w;
       const int64_t mine = (w < ncons && e0 < nmacro) ? (nmacro - e0 + W - 1) / W : 0;
@@ -128,7 +133,11 @@ struct Pipe {
       issued[w] = 0;
       nchunks[w] = (uint32_t)(mine * per);
       ps[w] = first_seg;
-      pq[w] = 0;
+      if (first_seg < nseg) {
+        src[w] = seg[first_seg].base + e0 * seg[first_seg].stride;
+        rem[w] = seg[first_seg].nch;
+        pol[w] = seg[first_seg].keep ? pol_last : pol_first;
+      }
     }
     // Round-robin over the consumer rings, one chunk per ring per round,
     // blocking (try_wait suspends in hardware) on the slot it needs next:
@@ -140,25 +149,27 @@ struct Pipe {
         const uint32_t c = issued[w];
         if (c >= nchunks[w]) continue;
         any = true;
-        const int slot = (int)(c % S);
+        const uint32_t slot = c % S;
         if (c >= S)
           while (!mbar_try_wait(&empty[w * S + slot], ((c / S) - 1) & 1u)) {
           }
-        const Segment& sg = seg[ps[w]];
         mbar_expect_tx(&full[w * S + slot], CH * 8u);
-        bulk_g2s(rings + (size_t)w * RING + slot * CH,
-                 sg.base + pe[w] * sg.stride + (int64_t)pq[w] * CH, CH * 8u,
-                 &full[w * S + slot], sg.keep ? pol_last : pol_first);
-        if (++pq[w] == sg.nch) {
-          pq[w] = 0;
+        bulk_g2s(rings + (size_t)w * RING + slot * CH, src[w], CH * 8u, &full[w * S + slot],
+                 pol[w]);
+        src[w] += CH;
+        issued[w] = c + 1;
+        if (--rem[w] == 0) {
           do {
             if (++ps[w] == nseg) {
               ps[w] = 0;
               pe[w] += W;
             }
           } while (seg[ps[w]].nch == 0);
+          const Segment& sg = seg[ps[w]];
+          src[w] = sg.base + pe[w] * sg.stride;
+          rem[w] = sg.nch;
+          pol[w] = sg.keep ? pol_last : pol_first;
         }
-        issued[w] = c + 1;
       }
       if (!any) break;
     }
