@@ -14,7 +14,10 @@ from pathlib import Path
 import numpy as np
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libmehdg_b200.so"
+# MEHDG_LIB_VARIANT=x loads libmehdg_b200.x.so instead (A/B builds of a kernel
+# design point measured on the same box; tools/ only)
+_VARIANT = os.environ.get("MEHDG_LIB_VARIANT")
+LIB_PATH = _PKG / (f"libmehdg_b200.{_VARIANT}.so" if _VARIANT else "libmehdg_b200.so")
 
 MH_OK = 0
 MH_E_ARG = -1

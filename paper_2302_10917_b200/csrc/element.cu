@@ -37,8 +37,15 @@
 namespace mh {
 namespace {
 
-constexpr int kWPB = 4;                 // consumer warps (macros in flight) per CTA
-constexpr int kThreads = (kWPB + 1) * 32;  // + one producer warp
+// Consumer warps (macros in flight) per CTA, plus one producer warp; 12 / kWPB
+// CTAs per SM.  3 + 1 warps at 4 CTAs/SM (12 consumers, 4 producers per SM)
+// measured 5.52 TB/s at c2 against 5.32 for 4 + 1 at 3 CTAs/SM (same box);
+// 2 + 1 at 6 CTAs/SM (96 registers) 4.75.
+#ifndef MH_ELEM_WPB
+#define MH_ELEM_WPB 3
+#endif
+constexpr int kWPB = MH_ELEM_WPB;
+constexpr int kThreads = (kWPB + 1) * 32;
 
 struct ElemArgs {
   const int32_t* elem_ufac;
@@ -160,7 +167,7 @@ __device__ __forceinline__ double dot_row(const double (&y)[R], const double* ri
 }
 
 template <int R, int MODE, int RING, int CH>
-__global__ void __launch_bounds__(kThreads, 3)
+__global__ void __launch_bounds__(kThreads, 12 / kWPB)
 element_kernel(ElemArgs a) {
   constexpr int S = RING / CH;
   using PipeT = Pipe<RING, CH, kWPB>;
@@ -429,9 +436,10 @@ int launch_rc(mh_system* s, const ElemArgs& a) {
 
 template <int R, int MODE>
 int launch_rm(mh_system* s, const ElemArgs& a) {
-  // 16 KB rings of four 4 KB chunks, 3 CTAs = 12 consumer warps per SM.
-  // Measured alternatives at c2: 8 KB rings of 2 KB chunks at 4 CTAs/SM
-  // -13%, 12 KB rings of three 4 KB chunks at 4 CTAs/SM -1.5%.
+  // 16 KB rings of four 4 KB chunks, 12 consumer warps per SM.  Measured
+  // alternatives at c2: 8 KB rings of 2 KB chunks at 16 consumers/SM -13%,
+  // 12 KB rings of three 4 KB chunks -1.5%, 2 KB / 1 KB chunks (MEHDG_ELEM_CH)
+  // -22% / -57%.
   const char* cv = getenv("MEHDG_ELEM_CH");
   const int ch = cv ? atoi(cv) : 512;
   if (ch == 256) return launch_rc<R, MODE, 2048, 256>(s, a);
