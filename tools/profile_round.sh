@@ -23,4 +23,12 @@ ncu --set full --import-source on --clock-control none -k regex:assemble_macro -
 python tools/asm_probe.py 128 2 3 3 > $out/asm_probe.txt 2>&1
 for c in c2 c3 c5n20; do python tools/lu_probe.py $c 4 >> $out/lu_probe.txt 2>&1; done
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/fp64_peak tools/fp64_peak.cu && ./tools/fp64_peak > $out/fp64_peak.txt 2>&1
+# summaries on the box (the .ncu-rep files exceed gpurun's 64 MiB copy-back);
+# only the element-kernel c2 report travels back
+for r in $out/*.ncu-rep; do
+  python tools/ncu_hot.py $r "" 30 > ${r%.ncu-rep}_hot.txt 2>&1
+  python profiles/ncu_summary.py $r 0 > ${r%.ncu-rep}_sum.txt 2>&1
+  ncu -i $r --page raw --csv --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum > ${r%.ncu-rep}_dram.csv 2>/dev/null
+done
+find $out -name "*.ncu-rep" ! -name element_c2.ncu-rep -delete
 ls -la $out
