@@ -44,6 +44,12 @@ namespace {
 #ifndef MH_ELEM_WPB
 #define MH_ELEM_WPB 3
 #endif
+#ifndef MH_ELEM_MINB
+#define MH_ELEM_MINB (12 / MH_ELEM_WPB)
+#endif
+#ifndef MH_ELEM_RING
+#define MH_ELEM_RING 2048
+#endif
 constexpr int kWPB = MH_ELEM_WPB;
 constexpr int kThreads = (kWPB + 1) * 32;
 
@@ -167,7 +173,7 @@ __device__ __forceinline__ double dot_row(const double (&y)[R], const double* ri
 }
 
 template <int R, int MODE, int RING, int CH>
-__global__ void __launch_bounds__(kThreads, 12 / kWPB)
+__global__ void __launch_bounds__(kThreads, MH_ELEM_MINB)
 element_kernel(ElemArgs a) {
   constexpr int S = RING / CH;
   using PipeT = Pipe<RING, CH, kWPB>;
@@ -442,9 +448,9 @@ int launch_rm(mh_system* s, const ElemArgs& a) {
   // -22% / -57%.
   const char* cv = getenv("MEHDG_ELEM_CH");
   const int ch = cv ? atoi(cv) : 512;
-  if (ch == 256) return launch_rc<R, MODE, 2048, 256>(s, a);
-  if (ch == 128) return launch_rc<R, MODE, 2048, 128>(s, a);
-  return launch_rc<R, MODE, 2048, 512>(s, a);
+  if (ch == 256) return launch_rc<R, MODE, MH_ELEM_RING, 256>(s, a);
+  if (ch == 128) return launch_rc<R, MODE, MH_ELEM_RING, 128>(s, a);
+  return launch_rc<R, MODE, MH_ELEM_RING, 512>(s, a);
 }
 
 template <int MODE>
