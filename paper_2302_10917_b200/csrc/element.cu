@@ -427,9 +427,24 @@ int launch_rc(mh_system* s, const ElemArgs& a) {
   static_assert(kStreamChunk % CH == 0, "HBM padding must be a multiple of the ring chunk");
   const size_t smem = smem_bytes<RING, CH>(s->nc);
   auto kern = element_kernel<R, MODE, RING, CH>;
-  MH_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int per_sm = 0;
-  MH_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
+  // attribute + occupancy are host-side driver calls (microseconds): once per
+  // instantiation and shared-memory size, not per apply (GMRES launches an
+  // apply per Arnoldi step right after a host round trip)
+  struct Occ {
+    int dev = -1;
+    size_t smem = 0;
+    int per_sm = 0;
+  };
+  static thread_local Occ occ;
+  if (occ.dev != s->device || occ.smem != smem) {
+    MH_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    MH_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
+    occ.dev = s->device;
+    occ.smem = smem;
+    occ.per_sm = per_sm;
+  }
+  int per_sm = occ.per_sm;
   if (per_sm < 1) per_sm = 1;
   if (const char* v = getenv("MEHDG_ELEM_CTAS")) per_sm = std::max(1, std::min(per_sm, atoi(v)));
   int64_t grid = (int64_t)s->num_sms * per_sm;

@@ -77,8 +77,29 @@ __global__ void __launch_bounds__(kFaceWarps * 32) face_reduce_kernel(FaceArgs a
     const int i = lane + 32 * r;
     z[r] = i < t ? __ldg((RHS ? a.Rhat : a.uhat) + f * t + i) : 0.0;
   }
-  if (!RHS) warp_gemv<RT>(z, a.D + f * TT, t, sw, lane);  // D_f uhat_f
   const int sl = __ldg(a.vslot + 2 * f), sr = __ldg(a.vslot + 2 * f + 1);
+  if (PRE && !RHS) {
+    // M(A u)_f = D_f^-1 (D_f u_f - v_L - v_R) = u_f - D_f^-1 (v_L + v_R): the
+    // same operator reading only D_f^-1 (one t x t block per face, not two)
+    double q[RT];
+#pragma unroll
+    for (int r = 0; r < RT; ++r) {
+      const int i = lane + 32 * r;
+      q[r] = 0.0;
+      if (i < t) {
+        if (sl >= 0) q[r] = __ldg(a.V + (int64_t)sl * t + i);
+        if (sr >= 0) q[r] += __ldg(a.V + (int64_t)sr * t + i);
+      }
+    }
+    warp_gemv<RT>(q, a.Dinv + f * TT, t, sw, lane);
+#pragma unroll
+    for (int r = 0; r < RT; ++r) {
+      const int i = lane + 32 * r;
+      if (i < t) a.out[f * t + i] = z[r] - q[r];
+    }
+    return;
+  }
+  if (!RHS) warp_gemv<RT>(z, a.D + f * TT, t, sw, lane);  // D_f uhat_f
 #pragma unroll
   for (int r = 0; r < RT; ++r) {
     const int i = lane + 32 * r;
@@ -111,6 +132,23 @@ __global__ void __launch_bounds__(kFaceWarps * 32) face_small_kernel(FaceArgs a)
   double* su = s_u + grp * G;
   double z = row ? __ldg((RHS ? a.Rhat : a.uhat) + f * t + g) : 0.0;
   const unsigned mask = G == 32 ? kFull : (0xffffu << (tid & 16));
+  if (PRE && !RHS) {  // u_f - D_f^-1 (v_L + v_R), see face_reduce_kernel
+    double q = 0.0;
+    if (row) {
+      const int sl = __ldg(a.vslot + 2 * f), sr = __ldg(a.vslot + 2 * f + 1);
+      if (sl >= 0) q = __ldg(a.V + (int64_t)sl * t + g);
+      if (sr >= 0) q += __ldg(a.V + (int64_t)sr * t + g);
+    }
+    su[g] = q;
+    __syncwarp(mask);
+    const double* Mi = a.Dinv + (valid_face ? f : 0) * TT;
+    double acc = 0.0;
+#pragma unroll
+    for (int s = 0; s < G; ++s)
+      if (s < t && row) acc = fma(__ldg(Mi + (size_t)s * t + g), su[s], acc);
+    if (row) a.out[f * t + g] = z - acc;
+    return;
+  }
   if (!RHS) {
     su[g] = z;
     __syncwarp(mask);
