@@ -37,6 +37,10 @@ import numpy as np
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
+# NCCL's own log lines (e.g. "NCCL version ...") go to stderr: stdout carries the
+# one JSON line
+os.environ.setdefault("NCCL_DEBUG", "WARN")
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
 BASELINE_METRIC = "Schur-operator applies/sec & HBM GB/s (% roofline); batched LU GFLOP/s fp64"
 UNIT = "applies/s"
@@ -128,11 +132,11 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # distributed plumbing
 
-def dist_setup():
+def dist_setup(slabs: bool = False):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world > 1 or slabs:
         import torch
         import torch.distributed as dist
 
@@ -213,14 +217,14 @@ def time_oracle(prob: dict, n_macros: int, reps: int, threads: int):
 
 # ---------------------------------------------------------------------------
 
-def config_block(name, prob, world):
+def config_block(name, prob, world, slabs=False):
     return {"workload": f"BASELINE {name}: d={prob['d']} n={prob['n']} m={prob['m']} "
                         f"p={prob['p']} fp64 seed={prob['seed']}",
             "N_macros": prob["N"], "Q": prob["Q"], "t": prob["t"], "nc": prob["nc"],
             "F_unknown": prob["F"], "zhat": prob["zhat"],
             "operator": "matrix-free D - C A^-1 B (C = B^T synthetic, B_e streamed once)",
             "l2_flush": "none needed: 3.2 GB of blocks per apply >> 126 MB L2",
-            "parallelism": f"slabs{world} (NCCL halo)" if world > 1 else "single"}
+            "parallelism": f"slabs{world} (NCCL halo)" if (world > 1 or slabs) else "single"}
 
 
 _REF_PROB = None  # the workload, inherited by the forked reference workers
@@ -299,7 +303,7 @@ def build_local(args, world, rank, dev):
 
     d, n, m, p = S.CONFIGS[args.config]
     t0 = time.perf_counter()
-    if world == 1:
+    if world == 1 and not args.slabs:
         prob = S.make_problem(d, n, m, p, seed=args.seed)
         t_gen = time.perf_counter() - t0
         tables = {"nfe": d + 1, "elem_ufac": prob["elem_face"], "face_elem": prob["face_elem"],
@@ -547,7 +551,7 @@ def run_ours(args, world, rank, local):
         "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded BASELINE generator, numpy PCG64; blocks resident in HBM)",
-        "config": config_block(args.config, prob, world),
+        "config": config_block(args.config, prob, world, plan is not None),
         "hbm_gbs": bytes_apply / (ms_per_step * 1e-3) / 1e9,
         "hbm_frac": bytes_apply / (ms_per_step * 1e-3) / 1e9 / (peaks["hbm_gbs"] * world),
         "bytes_per_apply": bytes_apply,
@@ -598,6 +602,9 @@ def main():
     ap.add_argument("--cpu-reps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-mb", action="store_true", help="skip the matrix-based mode timing")
+    ap.add_argument("--slabs", action="store_true",
+                    help="take the multi-rank path (RankSystem, NCCL communicator) even on "
+                         "one rank; launch under torchrun")
     ap.add_argument("--no-asm", action="store_true",
                     help="skip the device HDG assembly / real-problem solve timing")
     args = ap.parse_args()
@@ -607,11 +614,11 @@ def main():
         world = int(os.environ.get("WORLD_SIZE", "1"))
         rank = int(os.environ.get("RANK", "0"))
         return run_reference(args, world, rank)
-    world, rank, local = dist_setup()
+    world, rank, local = dist_setup(args.slabs)
     try:
         return run_ours(args, world, rank, local)
     finally:
-        if world > 1:
+        if world > 1 or args.slabs:
             import torch.distributed as dist
 
             dist.destroy_process_group()

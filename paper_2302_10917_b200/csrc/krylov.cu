@@ -182,7 +182,7 @@ thread_local mh_system* g_comm_sys = nullptr;  // bound for the duration of one 
 
 int dot_dev(cudaStream_t st, Krylov* K, int64_t n, double* w, const double* Vp,
             const double* coef, const double* Vi, int mode, double* out) {
-  const bool multi = g_comm_sys && g_comm_sys->nranks > 1;
+  const bool multi = g_comm_sys && (g_comm_sys->nranks > 1 || g_comm_sys->nccl);
   dot_kernel<<<kDotBlocks, kDotThreads, 0, st>>>(n, w, Vp, coef, Vi, mode, !multi, K->part.p,
                                                   K->ticket.p, multi ? K->scal.p + 3 : out);
   MH_CHECK_CUDA(cudaGetLastError());
@@ -297,7 +297,8 @@ int gmres_core(cudaStream_t st, Krylov* K, int64_t n, const OpFn& A, const OpFn&
   }
   const int m = restart;
   const char* gv = getenv("MEHDG_GMRES_GRAPHS");
-  const bool use_graphs = K->persistent && !(g_comm_sys && g_comm_sys->nranks > 1) &&
+  const bool use_graphs = K->persistent &&
+                          !(g_comm_sys && (g_comm_sys->nranks > 1 || g_comm_sys->nccl)) &&
                           !(gv && gv[0] == '0');
   std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), y(m);
   auto Hat = [&](int i, int k) -> double& { return H[(size_t)i * m + k]; };

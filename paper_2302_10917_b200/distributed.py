@@ -59,7 +59,9 @@ class RankSystem:
                               ptr(_i32(plan.send_count)), ptr(_i32(plan.recv_count)),
                               ptr(_i32(plan.vret_slot)), ptr(_i32(plan.vret_count)),
                               ptr(_i32(plan.vrecv_count))), "mh_set_halo")
-        self.has_comm = comm_id is not None and plan.nranks > 1
+        # a communicator is used whenever one is given (with one rank too: the
+        # NCCL calls then run on a single-GPU box, tests/test_gpu_multislab.py)
+        self.has_comm = comm_id is not None
         if self.has_comm:
             idb = C.create_string_buffer(comm_id, 128)
             check(lib.mh_comm_init(h, idb, plan.nranks, plan.rank), "mh_comm_init")

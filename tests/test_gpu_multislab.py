@@ -12,7 +12,7 @@ import torch
 
 import paper_2302_10917_b200 as P
 from paper_2302_10917_b200 import synthetic as S
-from paper_2302_10917_b200.distributed import RankSystem, group_apply, local_trace
+from paper_2302_10917_b200.distributed import RankSystem, group_apply, local_trace, nccl_unique_id
 from paper_2302_10917_b200.partition import partition, rank_plan
 
 pytestmark = pytest.mark.gpu
@@ -56,3 +56,24 @@ def test_single_rank_plan_matches_plain_system(gpu):
     u = torch.as_tensor(prob["uhat"], device="cuda")
     assert torch.equal(rs.apply(u), P.apply_schur(ref, u))
     assert np.array_equal(rs.f_dev.cpu().numpy(), ref.f_vec)
+
+
+def test_single_rank_nccl_communicator(gpu):
+    """The NCCL path (dlopen, ncclCommInitRank, grouped halo calls, all-gathered
+    dot products, GMRES without graphs) on a one-rank communicator: bitwise the
+    plain single-GPU apply and solve."""
+    prob = S.make_problem(2, 8, 2, 3, seed=4)
+    pl = rank_plan(prob["elem_face"], prob["face_elem"], prob["face_slot"],
+                   np.array([0, prob["N"]]), 0)
+    rs = RankSystem(prob, pl, device=0, comm_id=nccl_unique_id())
+    assert rs.has_comm
+    ref = single_system(prob)
+    u = torch.as_tensor(prob["uhat"], device="cuda")
+    assert torch.equal(rs.apply(u), P.apply_schur(ref, u))
+    assert np.array_equal(rs.f_dev.cpu().numpy(), ref.f_vec)
+    x, info = rs.gmres(tol=1e-10)
+    xr, ir = P.gmres(P.SchurOperator(ref), ref.f_device, P.SolverConfig(tol=1e-10),
+                     precond=P.Preconditioner(ref))
+    assert info["converged"] and info["iterations"] == ir["iterations"]
+    xr = xr.cpu().numpy() if hasattr(xr, "cpu") else np.asarray(xr)
+    assert np.array_equal(x.cpu().numpy(), xr)
