@@ -7,6 +7,8 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "mh_internal.h"
 
@@ -241,6 +243,105 @@ static int alloc_blocks(mh_system* s) {
   return MH_OK;
 }
 
+// ---- host -> device uploads of the (GB-sized) blocks -------------------------
+// A pageable cudaMemcpy runs at host-memcpy speed through the driver's single
+// staging thread.  Large uploads instead go through pinned staging buffers:
+// T host threads each copy their contiguous slice chunk by chunk into two pinned
+// buffers of their own and issue the H2D copies on their own stream, so the
+// CPU copies of chunk i+1 overlap the PCIe transfer of chunk i.  The pinned
+// buffers, streams and events are created once per device and kept.
+namespace {
+constexpr size_t kStageChunk = (size_t)8 << 20;
+constexpr size_t kStageMin = (size_t)32 << 20;  // below this: plain cudaMemcpyAsync
+struct HostStage {
+  std::mutex mu;
+  int nthr = 0;
+  std::vector<void*> buf;        // 2 per thread
+  std::vector<cudaStream_t> st;  // 1 per thread
+  std::vector<cudaEvent_t> ev;   // 2 per thread
+};
+HostStage g_stage[16];
+
+int stage_init(HostStage& hs, int device) {
+  if (hs.nthr) return MH_OK;
+  const unsigned hc = std::thread::hardware_concurrency();
+  int n = (int)std::max(1u, std::min(16u, hc ? hc : 1u));
+  if (const char* v = getenv("MEHDG_UPLOAD_THREADS")) n = std::max(1, std::min(32, atoi(v)));
+  MH_CHECK_CUDA(cudaSetDevice(device));
+  for (int i = 0; i < n; ++i) {
+    cudaStream_t st;
+    MH_CHECK_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    hs.st.push_back(st);
+    for (int b = 0; b < 2; ++b) {
+      void* p = nullptr;
+      MH_CHECK_CUDA(cudaHostAlloc(&p, kStageChunk, cudaHostAllocDefault));
+      hs.buf.push_back(p);
+      cudaEvent_t ev;
+      MH_CHECK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      hs.ev.push_back(ev);
+    }
+  }
+  hs.nthr = n;
+  return MH_OK;
+}
+}  // namespace
+
+// bytes from host memory `src` to device memory `dst`; returns after the copy
+// has completed (earlier work on the system stream is drained first)
+static int h2d(mh_system* s, void* dst, const void* src, size_t bytes) {
+  if (!bytes) return MH_OK;
+  if (bytes < kStageMin || s->device < 0 || s->device >= 16) {
+    MH_CHECK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s->stream));
+    MH_CHECK_CUDA(cudaStreamSynchronize(s->stream));
+    return MH_OK;
+  }
+  HostStage& hs = g_stage[s->device];
+  std::lock_guard<std::mutex> lk(hs.mu);
+  MH_CHECK(stage_init(hs, s->device));
+  MH_CHECK_CUDA(cudaStreamSynchronize(s->stream));
+  const int n = hs.nthr;
+  const size_t per = ((bytes + n - 1) / n + 4095) & ~(size_t)4095;
+  std::vector<int> status((size_t)n, MH_OK);
+  std::vector<std::string> err((size_t)n);
+  auto work = [&](int i) {
+    cudaSetDevice(s->device);
+    const size_t b0 = std::min(bytes, (size_t)i * per), b1 = std::min(bytes, b0 + per);
+    int k = 0;
+    for (size_t off = b0; off < b1; off += kStageChunk, ++k) {
+      const size_t len = std::min(kStageChunk, b1 - off);
+      const int b = k & 1;
+      cudaError_t ce = cudaSuccess;
+      if (k >= 2) ce = cudaEventSynchronize(hs.ev[2 * i + b]);
+      if (ce == cudaSuccess) {
+        std::memcpy(hs.buf[2 * i + b], static_cast<const char*>(src) + off, len);
+        ce = cudaMemcpyAsync(static_cast<char*>(dst) + off, hs.buf[2 * i + b], len,
+                             cudaMemcpyHostToDevice, hs.st[i]);
+      }
+      if (ce == cudaSuccess) ce = cudaEventRecord(hs.ev[2 * i + b], hs.st[i]);
+      if (ce != cudaSuccess) {
+        status[i] = MH_E_CUDA;
+        err[i] = cudaGetErrorString(ce);
+        return;
+      }
+    }
+    const cudaError_t ce = cudaStreamSynchronize(hs.st[i]);
+    if (ce != cudaSuccess) {
+      status[i] = MH_E_CUDA;
+      err[i] = cudaGetErrorString(ce);
+    }
+  };
+  std::vector<std::thread> th;
+  for (int i = 1; i < n; ++i) th.emplace_back(work, i);
+  work(0);
+  for (auto& x : th) x.join();
+  for (int i = 0; i < n; ++i)
+    if (status[i] != MH_OK) {
+      set_error("staged upload: " + err[i]);
+      return status[i];
+    }
+  return MH_OK;
+}
+
 static int upload_impl(mh_system* s, const double* A, const double* B, const double* C,
                        const double* Ru, const double* D, const double* Rhat,
                        cudaMemcpyKind kind) {
@@ -252,20 +353,41 @@ static int upload_impl(mh_system* s, const double* A, const double* B, const dou
   MH_CHECK(alloc_blocks(s));
   const size_t N = (size_t)s->N, Q = s->Q, nc = s->nc, F = (size_t)s->F, t = s->t;
   cudaStream_t st = s->stream;
-  if (N) MH_CHECK_CUDA(cudaMemcpyAsync(s->A.p, A, sizeof(double) * N * Q * Q, kind, st));
+  const bool host = kind == cudaMemcpyHostToDevice;
+  // contiguous copies: staged through pinned buffers from host memory
+  auto copy = [&](void* dst, const void* src, size_t bytes) -> int {
+    if (host) return h2d(s, dst, src, bytes);
+    if (bytes) MH_CHECK_CUDA(cudaMemcpyAsync(dst, src, bytes, kind, st));
+    return MH_OK;
+  };
+  if (N) MH_CHECK(copy(s->A.p, A, sizeof(double) * N * Q * Q));
   s->c_is_bt = (B == nullptr) || (C == nullptr);
   if (!s->c_is_bt) MH_CHECK(s->Cm.alloc(N * (size_t)s->ldB));
   else s->Cm.release();
   const size_t row = sizeof(double) * nc * Q, pitch = sizeof(double) * (size_t)s->ldB;
   if (N && (size_t)s->ldB != nc * Q)  // zero the per-macro pad (streamed, never used)
     MH_CHECK_CUDA(cudaMemsetAsync(s->Bt.p, 0, pitch * N, st));
+  // a (N x rows) block with host row length `row` into device pitch `pitch`:
+  // contiguous upload to the staging buffer, then a device-side pitched copy
+  auto copy_pitched = [&](double* dst, const double* src) -> int {
+    if (!host) {
+      MH_CHECK_CUDA(cudaMemcpy2DAsync(dst, pitch, src, row, row, N, kind, st));
+      return MH_OK;
+    }
+    MH_CHECK(s->S.alloc(N * nc * Q));
+    MH_CHECK(h2d(s, s->S.p, src, row * N));
+    MH_CHECK_CUDA(cudaMemcpy2DAsync(dst, pitch, s->S.p, row, row, N, cudaMemcpyDeviceToDevice, st));
+    MH_CHECK_CUDA(cudaStreamSynchronize(st));
+    s->S.release();
+    return MH_OK;
+  };
   if (B == nullptr) {
-    if (N) MH_CHECK_CUDA(cudaMemcpy2DAsync(s->Bt.p, pitch, C, row, row, N, kind, st));
+    if (N) MH_CHECK(copy_pitched(s->Bt.p, C));
   } else {
     // op.B (N x Q x nc) -> Bt (N x nc x Q, stride ldB) through a staging buffer
     if (N) {
       MH_CHECK(s->S.alloc(N * nc * Q));
-      MH_CHECK_CUDA(cudaMemcpyAsync(s->S.p, B, row * N, kind, st));
+      MH_CHECK(copy(s->S.p, B, row * N));
       MH_CHECK(launch_transpose_batched(st, s->S.p, s->Bt.p, (int64_t)N, (int)Q, (int)nc,
                                         s->ldB));
       MH_CHECK_CUDA(cudaStreamSynchronize(st));
@@ -273,16 +395,16 @@ static int upload_impl(mh_system* s, const double* A, const double* B, const dou
     }
     if (C && N) {
       MH_CHECK_CUDA(cudaMemsetAsync(s->Cm.p, 0, pitch * N, st));
-      MH_CHECK_CUDA(cudaMemcpy2DAsync(s->Cm.p, pitch, C, row, row, N, kind, st));
+      MH_CHECK(copy_pitched(s->Cm.p, C));
     }
   }
   if (N) {
-    if (Ru) MH_CHECK_CUDA(cudaMemcpyAsync(s->Ru.p, Ru, sizeof(double) * N * Q, kind, st));
+    if (Ru) MH_CHECK(copy(s->Ru.p, Ru, sizeof(double) * N * Q));
     else MH_CHECK_CUDA(cudaMemsetAsync(s->Ru.p, 0, sizeof(double) * N * Q, st));
   }
   if (F) {
-    MH_CHECK_CUDA(cudaMemcpyAsync(s->Draw.p, D, sizeof(double) * F * t * t, kind, st));
-    if (Rhat) MH_CHECK_CUDA(cudaMemcpyAsync(s->Rhat.p, Rhat, sizeof(double) * F * t, kind, st));
+    MH_CHECK(copy(s->Draw.p, D, sizeof(double) * F * t * t));
+    if (Rhat) MH_CHECK(copy(s->Rhat.p, Rhat, sizeof(double) * F * t));
     else MH_CHECK_CUDA(cudaMemsetAsync(s->Rhat.p, 0, sizeof(double) * F * t, st));
   }
   MH_CHECK_CUDA(cudaMemsetAsync(s->V.p, 0, sizeof(double) * s->V.n, st));
