@@ -251,7 +251,7 @@ static int alloc_blocks(mh_system* s) {
 // CPU copies of chunk i+1 overlap the PCIe transfer of chunk i.  The pinned
 // buffers, streams and events are created once per device and kept.
 namespace {
-constexpr size_t kStageChunk = (size_t)8 << 20;
+constexpr size_t kStageChunk = (size_t)4 << 20;
 constexpr size_t kStageMin = (size_t)32 << 20;  // below this: plain cudaMemcpyAsync
 struct HostStage {
   std::mutex mu;
@@ -268,19 +268,25 @@ int stage_init(HostStage& hs, int device) {
   int n = (int)std::max(1u, std::min(16u, hc ? hc : 1u));
   if (const char* v = getenv("MEHDG_UPLOAD_THREADS")) n = std::max(1, std::min(32, atoi(v)));
   MH_CHECK_CUDA(cudaSetDevice(device));
-  for (int i = 0; i < n; ++i) {
-    cudaStream_t st;
-    MH_CHECK_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    hs.st.push_back(st);
-    for (int b = 0; b < 2; ++b) {
-      void* p = nullptr;
-      MH_CHECK_CUDA(cudaHostAlloc(&p, kStageChunk, cudaHostAllocDefault));
-      hs.buf.push_back(p);
-      cudaEvent_t ev;
-      MH_CHECK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-      hs.ev.push_back(ev);
+  hs.st.assign(n, nullptr);
+  hs.buf.assign(2 * n, nullptr);
+  hs.ev.assign(2 * n, nullptr);
+  // page-locking is the slow part of the first upload: the threads do it in parallel
+  std::vector<cudaError_t> res(n, cudaSuccess);
+  auto mk = [&](int i) {
+    cudaError_t ce = cudaSetDevice(device);
+    if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&hs.st[i], cudaStreamNonBlocking);
+    for (int b = 0; b < 2 && ce == cudaSuccess; ++b) {
+      ce = cudaHostAlloc(&hs.buf[2 * i + b], kStageChunk, cudaHostAllocDefault);
+      if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&hs.ev[2 * i + b], cudaEventDisableTiming);
     }
-  }
+    res[i] = ce;
+  };
+  std::vector<std::thread> th;
+  for (int i = 1; i < n; ++i) th.emplace_back(mk, i);
+  mk(0);
+  for (auto& x : th) x.join();
+  for (int i = 0; i < n; ++i) MH_CHECK_CUDA(res[i]);
   hs.nthr = n;
   return MH_OK;
 }
@@ -290,7 +296,8 @@ int stage_init(HostStage& hs, int device) {
 // has completed (earlier work on the system stream is drained first)
 static int h2d(mh_system* s, void* dst, const void* src, size_t bytes) {
   if (!bytes) return MH_OK;
-  if (bytes < kStageMin || s->device < 0 || s->device >= 16) {
+  static const bool staged = !(getenv("MEHDG_UPLOAD_STAGE") && atoi(getenv("MEHDG_UPLOAD_STAGE")) == 0);
+  if (!staged || bytes < kStageMin || s->device < 0 || s->device >= 16) {
     MH_CHECK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s->stream));
     MH_CHECK_CUDA(cudaStreamSynchronize(s->stream));
     return MH_OK;
