@@ -49,3 +49,35 @@ def test_lu_matches_lapack_across_sizes(Q):
     o = SO.system_from_problem(prob).factorize()
     u = np.random.default_rng(Q).standard_normal(sys_.zhat)
     assert rel(P.apply_schur(sys_, u), o.apply(u)) <= 1e-10
+
+
+def test_staged_upload_large_blocks():
+    """Block arrays above the pinned-staging threshold (32 MB: the threaded,
+    chunked host -> device path of mh_upload_blocks) arrive intact: factors of
+    sampled macro match LAPACK and the apply matches the oracle on a mesh whose
+    A (217 MB) and op.C (51 MB, the pitched path) are not multiples of the 4 MB
+    chunks or of the per-thread slices."""
+    d, n, m, p = 2, 32, 2, 4  # N = 2048 macros, nc = 27
+    prob = S.make_problem(d, n, m, p, seed=17)
+    rng = np.random.default_rng(17)
+    N, Q, nc = prob["N"], prob["Q"], prob["nc"]
+    Qb = 115  # larger blocks
+    prob["Q"] = Qb
+    prob["A"] = rng.standard_normal((N, Qb, Qb)) + Qb * np.eye(Qb)
+    prob["Be"] = rng.standard_normal((N, nc, Qb))
+    prob["B"] = prob["Be"].transpose(0, 2, 1)
+    prob["C"] = prob["Be"]
+    prob["R_u"] = rng.standard_normal((N, Qb))
+    assert prob["A"].nbytes > 32 << 20 and prob["Be"].nbytes > 32 << 20
+    tables = {"nfe": 3, "elem_ufac": prob["elem_face"], "face_elem": prob["face_elem"],
+              "face_slot": prob["face_slot"], "uidx": prob["uidx"], "F": prob["F"]}
+    sys_ = P.condense_arrays(prob["mesh"], prob["A"], None, prob["Be"], prob["R_u"], prob["D"],
+                             prob["R_hat"], P.SolverConfig(tol=1e-10), tables=tables)
+    lu, piv = P.local_factors(sys_)
+    for e in range(0, N, 37):
+        ref_lu, ref_piv = sla.lu_factor(prob["A"][e])
+        assert np.array_equal(piv[e], ref_piv), e
+        assert np.abs(lu[e] - ref_lu).max() <= 1e-11 * np.abs(ref_lu).max(), e
+    o = SO.system_from_problem(prob).factorize()
+    u = np.random.default_rng(3).standard_normal(sys_.zhat)
+    assert rel(P.apply_schur(sys_, u), o.apply(u)) <= 1e-12
