@@ -37,9 +37,11 @@ import numpy as np
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
-# NCCL's own log lines (e.g. "NCCL version ...") go to stderr: stdout carries the
-# one JSON line
-os.environ.setdefault("NCCL_DEBUG", "WARN")
+# stdout carries the one JSON line: NCCL's version banner (the image sets
+# NCCL_DEBUG=VERSION, which prints to stdout) is turned off, other NCCL log
+# lines go to stderr
+if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+    os.environ["NCCL_DEBUG"] = "WARN"
 os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
 BASELINE_METRIC = "Schur-operator applies/sec & HBM GB/s (% roofline); batched LU GFLOP/s fp64"

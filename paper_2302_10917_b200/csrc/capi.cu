@@ -157,6 +157,11 @@ extern "C" int mh_destroy(mh_system* s) {
     cudaStreamDestroy(s->cout);
     for (cudaEvent_t e : s->evp) cudaEventDestroy(e);
   }
+  if (s->kstream) {
+    cudaStreamDestroy(s->kstream);
+    cudaEventDestroy(s->ev_u);
+    cudaEventDestroy(s->ev_int);
+  }
   if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
   delete s;
   return MH_OK;
@@ -181,11 +186,14 @@ extern "C" int mh_upload_connectivity(mh_system* s, const int32_t* elem_ufac,
   }
   MH_CHECK_CUDA(cudaSetDevice(s->device));
   const int64_t ntrace = s->F + s->F_halo;
-  for (int64_t i = 0; i < s->N * s->nfe; ++i)
+  s->e_split = 0;  // one past the last macro that reads a received halo trace
+  for (int64_t i = 0; i < s->N * s->nfe; ++i) {
     if (elem_ufac[i] < -1 || elem_ufac[i] >= ntrace) {
       set_error("elem_ufac entry out of range");
       return MH_E_ARG;
     }
+    if (elem_ufac[i] >= s->F) s->e_split = i / s->nfe + 1;
+  }
   std::vector<int32_t> vslot((size_t)(2 * s->F));
   for (int64_t f = 0; f < s->F; ++f)
     for (int c = 0; c < 2; ++c) {
@@ -517,12 +525,41 @@ extern "C" int mh_rhs(mh_system* s, double* f) {
   return launch_face_reduce(s, nullptr, f, 1, 0);
 }
 
+// Element phase of an apply: the uhat halo exchange, then the element kernel.
+// On a multi-rank system the macros that read no received trace, [e_split, N),
+// run on a second stream while the halo exchange is in flight on the system
+// stream; the macros [0, e_split) follow the exchange (overlap the
+// interior-macro work with the halo).  Each macro's arithmetic is unchanged, so
+// the result is bitwise the same.  MEHDG_SPLIT_AT=k forces e_split = k (tests).
+static int apply_elements(mh_system* s, const double* u) {
+  int64_t split = s->e_split;
+  if (const char* v = getenv("MEHDG_SPLIT_AT")) split = std::min<int64_t>(s->N, atoll(v));
+  if (!multi_rank(s) || split >= s->N) {
+    MH_CHECK(halo_u_exchange(s, u, nullptr));
+    return launch_element(s, kApply, u, s->V.p);
+  }
+  if (!s->kstream) {
+    MH_CHECK_CUDA(cudaStreamCreateWithFlags(&s->kstream, cudaStreamNonBlocking));
+    MH_CHECK_CUDA(cudaEventCreateWithFlags(&s->ev_u, cudaEventDisableTiming));
+    MH_CHECK_CUDA(cudaEventCreateWithFlags(&s->ev_int, cudaEventDisableTiming));
+  }
+  // everything earlier on the system stream (u, and the previous apply's use of
+  // V) precedes the interior macros
+  MH_CHECK_CUDA(cudaEventRecord(s->ev_u, s->stream));
+  MH_CHECK_CUDA(cudaStreamWaitEvent(s->kstream, s->ev_u, 0));
+  MH_CHECK(launch_element_range(s, kApply, u, s->V.p, s->kstream, split, s->N));
+  MH_CHECK_CUDA(cudaEventRecord(s->ev_int, s->kstream));
+  MH_CHECK(halo_u_exchange(s, u, nullptr));
+  MH_CHECK(launch_element_range(s, kApply, u, s->V.p, s->stream, 0, split));
+  MH_CHECK_CUDA(cudaStreamWaitEvent(s->stream, s->ev_int, 0));
+  return MH_OK;
+}
+
 extern "C" int mh_apply(mh_system* s, const double* u, double* w) {
   MH_CHECK(ready(s));
-  MH_CHECK(halo_u_exchange(s, u, nullptr));
   cudaEvent_t ev;
   MH_CHECK(prof_begin(s, &ev));
-  MH_CHECK(launch_element(s, kApply, u, s->V.p));
+  MH_CHECK(apply_elements(s, u));
   MH_CHECK(prof_end(s, ev, 0));
   MH_CHECK(halo_v_exchange(s));
   MH_CHECK(prof_begin(s, &ev));
@@ -532,10 +569,9 @@ extern "C" int mh_apply(mh_system* s, const double* u, double* w) {
 
 extern "C" int mh_apply_precond(mh_system* s, const double* u, double* z) {
   MH_CHECK(ready(s));
-  MH_CHECK(halo_u_exchange(s, u, nullptr));
   cudaEvent_t ev;
   MH_CHECK(prof_begin(s, &ev));
-  MH_CHECK(launch_element(s, kApply, u, s->V.p));
+  MH_CHECK(apply_elements(s, u));
   MH_CHECK(prof_end(s, ev, 0));
   MH_CHECK(halo_v_exchange(s));
   MH_CHECK(prof_begin(s, &ev));

@@ -125,9 +125,7 @@ int exchange(mh_system* s, const double* sendbuf, const std::vector<int32_t>& sc
   return MH_OK;
 }
 
-// a system with a communicator takes the NCCL path even with one rank (the
-// single-GPU box's test of the NCCL calls); plain systems the no-op path
-bool multi(mh_system* s) { return s->nranks > 1 || s->nccl != nullptr; }
+bool multi(mh_system* s) { return multi_rank(s); }
 
 int need_comm(mh_system* s) {
   if (!s->have_halo || !s->nccl) {

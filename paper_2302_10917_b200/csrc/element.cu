@@ -66,6 +66,7 @@ struct ElemArgs {
   const double* Ru;
   double* out;
   int64_t N, F, ldB, ldL;
+  int64_t e_lo;  // macros [e_lo, N) are processed
   int Q, nc, t, nfe;
   int c_is_bt;
 };
@@ -202,7 +203,8 @@ element_kernel(ElemArgs a) {
   const int64_t W = (int64_t)gridDim.x * kWPB;
   if (w == kWPB) {  // producer warp
     if (lane == 0)
-      PipeT::produce(rings, full, empty, segs, nseg, (int64_t)blockIdx.x * kWPB, W, a.N, kWPB);
+      PipeT::produce(rings, full, empty, segs, nseg, a.e_lo + (int64_t)blockIdx.x * kWPB, W, a.N,
+                     kWPB);
     return;
   }
   const double* ring = rings + (size_t)w * RING;
@@ -252,7 +254,7 @@ element_kernel(ElemArgs a) {
       g_n[q] = v;
     }
   };
-  const int64_t e_first = (int64_t)blockIdx.x * kWPB + w;
+  const int64_t e_first = a.e_lo + (int64_t)blockIdx.x * kWPB + w;
   if (e_first < a.N) {
     load_meta(e_first);
     if (MODE != kRhs) gather_next();
@@ -423,7 +425,7 @@ size_t smem_bytes(int nc) {
 }
 
 template <int R, int MODE, int RING, int CH>
-int launch_rc(mh_system* s, const ElemArgs& a) {
+int launch_rc(mh_system* s, const ElemArgs& a, cudaStream_t st) {
   static_assert(kStreamChunk % CH == 0, "HBM padding must be a multiple of the ring chunk");
   const size_t smem = smem_bytes<RING, CH>(s->nc);
   auto kern = element_kernel<R, MODE, RING, CH>;
@@ -448,29 +450,30 @@ int launch_rc(mh_system* s, const ElemArgs& a) {
   if (per_sm < 1) per_sm = 1;
   if (const char* v = getenv("MEHDG_ELEM_CTAS")) per_sm = std::max(1, std::min(per_sm, atoi(v)));
   int64_t grid = (int64_t)s->num_sms * per_sm;
-  const int64_t need = (s->N + kWPB - 1) / kWPB;
+  const int64_t need = (a.N - a.e_lo + kWPB - 1) / kWPB;
   if (grid > need) grid = need;
-  kern<<<(unsigned)grid, kThreads, smem, s->stream>>>(a);
+  kern<<<(unsigned)grid, kThreads, smem, st>>>(a);
   MH_CHECK_CUDA(cudaGetLastError());
   return MH_OK;
 }
 
 template <int R, int MODE>
-int launch_rm(mh_system* s, const ElemArgs& a) {
+int launch_rm(mh_system* s, const ElemArgs& a, cudaStream_t st) {
   // 16 KB rings of four 4 KB chunks, 12 consumer warps per SM.  Measured
   // alternatives at c2: 8 KB rings of 2 KB chunks at 16 consumers/SM -13%,
   // 12 KB rings of three 4 KB chunks -1.5%, 2 KB / 1 KB chunks (MEHDG_ELEM_CH)
   // -22% / -57%.
   const char* cv = getenv("MEHDG_ELEM_CH");
   const int ch = cv ? atoi(cv) : 512;
-  if (ch == 256) return launch_rc<R, MODE, MH_ELEM_RING, 256>(s, a);
-  if (ch == 128) return launch_rc<R, MODE, MH_ELEM_RING, 128>(s, a);
-  return launch_rc<R, MODE, MH_ELEM_RING, 512>(s, a);
+  if (ch == 256) return launch_rc<R, MODE, MH_ELEM_RING, 256>(s, a, st);
+  if (ch == 128) return launch_rc<R, MODE, MH_ELEM_RING, 128>(s, a, st);
+  return launch_rc<R, MODE, MH_ELEM_RING, 512>(s, a, st);
 }
 
 template <int MODE>
-int launch_mode(mh_system* s, const double* uhat, double* out) {
-  if (s->N == 0) return MH_OK;
+int launch_mode(mh_system* s, const double* uhat, double* out, cudaStream_t st, int64_t e_lo,
+                int64_t e_hi) {
+  if (e_hi <= e_lo) return MH_OK;
   ElemArgs a;
   a.elem_ufac = s->elem_ufac.p;
   a.uhat = uhat;
@@ -483,7 +486,8 @@ int launch_mode(mh_system* s, const double* uhat, double* out) {
   a.perm = s->perm.p;
   a.Ru = s->Ru.p;
   a.out = out;
-  a.N = s->N;
+  a.N = e_hi;
+  a.e_lo = e_lo;
   a.F = s->F;
   a.ldB = s->ldB;
   a.ldL = s->ldL;
@@ -493,14 +497,14 @@ int launch_mode(mh_system* s, const double* uhat, double* out) {
   a.nfe = s->nfe;
   a.c_is_bt = s->c_is_bt ? 1 : 0;
   switch ((s->Q + 31) / 32) {
-    case 1: return launch_rm<1, MODE>(s, a);
-    case 2: return launch_rm<2, MODE>(s, a);
-    case 3: return launch_rm<3, MODE>(s, a);
-    case 4: return launch_rm<4, MODE>(s, a);
-    case 5: return launch_rm<5, MODE>(s, a);
-    case 6: return launch_rm<6, MODE>(s, a);
-    case 7: return launch_rm<7, MODE>(s, a);
-    case 8: return launch_rm<8, MODE>(s, a);
+    case 1: return launch_rm<1, MODE>(s, a, st);
+    case 2: return launch_rm<2, MODE>(s, a, st);
+    case 3: return launch_rm<3, MODE>(s, a, st);
+    case 4: return launch_rm<4, MODE>(s, a, st);
+    case 5: return launch_rm<5, MODE>(s, a, st);
+    case 6: return launch_rm<6, MODE>(s, a, st);
+    case 7: return launch_rm<7, MODE>(s, a, st);
+    case 8: return launch_rm<8, MODE>(s, a, st);
   }
   set_error("element kernel: Q > 256 unsupported");
   return MH_E_UNSUPPORTED;
@@ -508,18 +512,25 @@ int launch_mode(mh_system* s, const double* uhat, double* out) {
 
 }  // namespace
 
-int launch_element(mh_system* s, int mode, const double* uhat, double* out) {
+int launch_element_range(mh_system* s, int mode, const double* uhat, double* out,
+                         cudaStream_t st, int64_t e_lo, int64_t e_hi) {
   if (s->Q > 256 || s->nc > 256) {
     set_error("element kernel: Q and nc must be <= 256");
     return MH_E_UNSUPPORTED;
   }
+  e_lo = std::max<int64_t>(e_lo, 0);
+  e_hi = std::min<int64_t>(e_hi, s->N);
   switch (mode) {
-    case kApply: return launch_mode<kApply>(s, uhat, out);
-    case kRhs: return launch_mode<kRhs>(s, uhat, out);
-    case kRecon: return launch_mode<kRecon>(s, uhat, out);
+    case kApply: return launch_mode<kApply>(s, uhat, out, st, e_lo, e_hi);
+    case kRhs: return launch_mode<kRhs>(s, uhat, out, st, e_lo, e_hi);
+    case kRecon: return launch_mode<kRecon>(s, uhat, out, st, e_lo, e_hi);
   }
   set_error("bad element mode");
   return MH_E_ARG;
+}
+
+int launch_element(mh_system* s, int mode, const double* uhat, double* out) {
+  return launch_element_range(s, mode, uhat, out, s->stream, 0, s->N);
 }
 
 }  // namespace mh

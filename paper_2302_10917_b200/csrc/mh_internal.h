@@ -133,6 +133,11 @@ struct mh_system {
   // multi-GPU (comm.cu)
   int nranks = 1, rank = 0;
   void* nccl = nullptr;  // ncclComm_t
+  // macros [0, e_split) read received halo traces; [e_split, N) run on kstream
+  // while the halo exchange is in flight (mh_apply on a multi-rank system)
+  int64_t e_split = 0;
+  cudaStream_t kstream = nullptr;
+  cudaEvent_t ev_u = nullptr, ev_int = nullptr;
   bool have_halo = false;
   std::vector<int32_t> send_count, recv_count, vret_count, vrecv_count;  // per peer
   mh::DBuf<int32_t> send_face, vret_slot;
@@ -146,6 +151,12 @@ int launch_lu(mh_system* s, float* ms);
 // element.cu
 enum ElemMode { kApply = 0, kRhs = 1, kRecon = 2 };
 int launch_element(mh_system* s, int mode, const double* uhat, double* out);
+// a system with a communicator takes the NCCL path even with one rank (the
+// single-GPU box's test of the NCCL calls); plain systems the no-op path
+inline bool multi_rank(const mh_system* s) { return s->nranks > 1 || s->nccl != nullptr; }
+// macros [e_lo, e_hi) on stream st
+int launch_element_range(mh_system* s, int mode, const double* uhat, double* out,
+                         cudaStream_t st, int64_t e_lo, int64_t e_hi);
 int launch_element_schur(mh_system* s);
 int launch_element_mb(mh_system* s, const double* uhat);
 // face.cu

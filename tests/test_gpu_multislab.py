@@ -58,10 +58,15 @@ def test_single_rank_plan_matches_plain_system(gpu):
     assert np.array_equal(rs.f_dev.cpu().numpy(), ref.f_vec)
 
 
-def test_single_rank_nccl_communicator(gpu):
+@pytest.mark.parametrize("split", [None, 0, 37, 64])
+def test_single_rank_nccl_communicator(gpu, split, monkeypatch):
     """The NCCL path (dlopen, ncclCommInitRank, grouped halo calls, all-gathered
     dot products, GMRES without graphs) on a one-rank communicator: bitwise the
-    plain single-GPU apply and solve."""
+    plain single-GPU apply and solve.  `split` forces the interior / halo macro
+    split of the apply (macros [split, N) on the second stream, overlapping the
+    halo exchange; [0, split) after it)."""
+    if split is not None:
+        monkeypatch.setenv("MEHDG_SPLIT_AT", str(split))
     prob = S.make_problem(2, 8, 2, 3, seed=4)
     pl = rank_plan(prob["elem_face"], prob["face_elem"], prob["face_slot"],
                    np.array([0, prob["N"]]), 0)
