@@ -47,6 +47,9 @@ namespace {
 #ifndef MH_ELEM_MINB
 #define MH_ELEM_MINB (12 / MH_ELEM_WPB)
 #endif
+#ifndef MH_ELEM_G
+#define MH_ELEM_G 8  // L / U columns per ring-window check in the substitutions (4 when 8 Q does not fit)
+#endif
 #ifndef MH_ELEM_RING
 #define MH_ELEM_RING 2048
 #endif
@@ -319,15 +322,16 @@ element_kernel(ElemArgs a) {
       for (int jb = 0; jb < R; ++jb) {
         const int jend = min(jb * 32 + 32, Q - 1);
         int j0 = jb * 32;
-        for (; j0 + 4 <= jend; j0 += 4) {
-          const uint32_t span = (uint32_t)(4 * (Q - 1 - j0) - 6);
+        constexpr int G = (MH_ELEM_G > 4 && MH_ELEM_G * 32 * R <= (RING / CH - 1) * CH) ? MH_ELEM_G : 4;
+        for (; j0 + G <= jend; j0 += G) {
+          const uint32_t span = (uint32_t)(G * (Q - 1 - j0) - G * (G - 1) / 2);
           cs.window(p, p + span, lane);
           if (no_wrap<RING>(p - (uint32_t)(j0 + 1), span + (uint32_t)(j0 + 1) + 32u * R + 8u)) {
-            fwd_cols<R, 4, RING, false>(y, ring, p, jb, j0, Q, lane);
+            fwd_cols<R, G, RING, false>(y, ring, p, jb, j0, Q, lane);
             p += span;
           } else {
 #pragma unroll 1
-            for (int u = 0; u < 4; ++u) {  // rare: the group wraps around the ring end
+            for (int u = 0; u < G; ++u) {  // rare: the group wraps around the ring end
               fwd_cols<R, 1, RING, true>(y, ring, p, jb, j0 + u, Q, lane);
               p += (uint32_t)(Q - 1 - (j0 + u));
             }
@@ -348,15 +352,16 @@ element_kernel(ElemArgs a) {
 #pragma unroll
       for (int jb = R - 1; jb >= 0; --jb) {
         int j0 = min(jb * 32 + 31, Q - 1);
-        for (; j0 - 3 >= jb * 32; j0 -= 4) {
-          const uint32_t span = (uint32_t)(4 * j0 - 6);
+        constexpr int G = (MH_ELEM_G > 4 && MH_ELEM_G * 32 * R <= (RING / CH - 1) * CH) ? MH_ELEM_G : 4;
+        for (; j0 - (G - 1) >= jb * 32; j0 -= G) {
+          const uint32_t span = (uint32_t)(G * j0 - G * (G - 1) / 2);
           cs.window(p, p + span, lane);
           if (no_wrap<RING>(p, span + 32u * R + 8u)) {
-            bwd_cols<R, 4, RING, false>(y, dr, ring, p, jb, j0, lane);
+            bwd_cols<R, G, RING, false>(y, dr, ring, p, jb, j0, lane);
             p += span;
           } else {
 #pragma unroll 1
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < G; ++u) {
               bwd_cols<R, 1, RING, true>(y, dr, ring, p, jb, j0 - u, lane);
               p += (uint32_t)(j0 - u);
             }
