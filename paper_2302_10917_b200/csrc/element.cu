@@ -50,6 +50,9 @@ namespace {
 #ifndef MH_ELEM_G
 #define MH_ELEM_G 8  // L / U columns per ring-window check in the substitutions (4 when 8 Q does not fit)
 #endif
+#ifndef MH_ELEM_GR
+#define MH_ELEM_GR 8  // op.B^T / op.C rows per ring-window check in steps 1 and 3 (when 8 Q <= 800)
+#endif
 #ifndef MH_ELEM_RING
 #define MH_ELEM_RING 2048
 #endif
@@ -294,13 +297,22 @@ element_kernel(ElemArgs a) {
       for (int r = 0; r < R; ++r) acc[r] = 0.0;
       uint32_t p = base;
       int c = 0;
-      for (; c + 4 <= nc; c += 4, p += 4u * (uint32_t)Q) {  // step 1: x = B ue
-        cs.window(p, p + 4u * Q, lane);
-        if (!has_perm && no_wrap<RING>(p, 4u * Q + 32u * R)) {
-          gemv_rows<R, 4, RING, false, false>(acc, ring, p, Q, su + c, pr, lane);
+      constexpr int GR = (MH_ELEM_GR > 4 && MH_ELEM_GR * 32 * R <= (RING / CH - 1) * CH)
+                             ? MH_ELEM_GR : 4;  // rows per ring-window check
+      // 8-row groups only while they span at most ~half the ring slack (c2, c3;
+      // at Q = 165 most 8-row groups would wrap the ring end)
+      const bool rows8 = 8 * Q <= 800;
+      for (; rows8 && c + GR <= nc; c += GR, p += (uint32_t)(GR * Q)) {  // step 1: x = B ue
+        cs.window(p, p + (uint32_t)(GR * Q), lane);
+        if (!has_perm && no_wrap<RING>(p, (uint32_t)(GR * Q) + 32u * R)) {
+          gemv_rows<R, GR, RING, false, false>(acc, ring, p, Q, su + c, pr, lane);
         } else {
-          gemv_rows<R, 4, RING, true, true>(acc, ring, p, Q, su + c, pr, lane);
+          gemv_rows<R, GR, RING, true, true>(acc, ring, p, Q, su + c, pr, lane);
         }
+      }
+      for (; c + 4 <= nc; c += 4, p += 4u * (uint32_t)Q) {
+        cs.window(p, p + 4u * Q, lane);
+        gemv_rows<R, 4, RING, true, true>(acc, ring, p, Q, su + c, pr, lane);
       }
       for (; c < nc; ++c, p += (uint32_t)Q) {
         cs.window(p, p + Q, lane);
@@ -389,6 +401,18 @@ element_kernel(ElemArgs a) {
     for (int c0 = 0; c0 < nc; c0 += 8) {
       double pp[8];
       const int nrow = min(8, nc - c0);
+      constexpr bool G8 = MH_ELEM_GR >= 8 && 8 * 32 * R <= (RING / CH - 1) * CH;
+      if (G8 && nrow == 8 && 8 * Q <= 800) {  // one ring-window check for the 8 rows
+        cs.window(p, p + 8u * Q, lane);
+        if (no_wrap<RING>(p, 8u * Q + 32u * R)) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) pp[u] = dot_row<R, RING, false>(y, ring, p + u * Q, Q, lane);
+        } else {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) pp[u] = dot_row<R, RING, true>(y, ring, p + u * Q, Q, lane);
+        }
+        p += 8u * Q;
+      } else
 #pragma unroll
       for (int q0 = 0; q0 < 8; q0 += 4) {
         if (q0 + 4 <= nrow) {
