@@ -124,6 +124,58 @@ dot_kernel(int64_t n, double* __restrict__ w, const double* __restrict__ Vp,
   }
 }
 
+// The whole MGS block of Arnoldi step k in ONE CTA for short vectors (n <=
+// kSmallMgsN): the k + 2 dependent reductions are block reductions instead of
+// k + 2 grid launches (launch latency bounds them at this size).  Same
+// arithmetic per element as dot_kernel (w -= h V in two roundings, fma dots);
+// each thread owns the same indices in every pass, so the in-place updates
+// need no synchronisation beyond the reductions.
+constexpr int kSmallMgsThreads = 1024;
+constexpr int64_t kSmallMgsN = 1 << 16;
+
+__device__ __forceinline__ double block_sum_bcast(double v, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    double r = lane < kSmallMgsThreads / 32 ? red[lane] : 0.0;
+    for (int o = 16; o; o >>= 1) r += __shfl_xor_sync(kFull, r, o);
+    if (lane == 0) red[32] = r;
+  }
+  __syncthreads();
+  const double r = red[32];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kSmallMgsThreads)
+mgs_small_kernel(int64_t n, double* __restrict__ w, const double* __restrict__ V, int k,
+                 double* __restrict__ hcol, double* __restrict__ vnext) {
+  __shared__ double red[33];
+  double c = 0.0;
+  const double* Vp = nullptr;
+  for (int i = 0; i <= k + 1; ++i) {
+    const double* Vi = V + (size_t)i * n;  // i = k + 1: the norm of w
+    double acc = 0.0;
+    for (int64_t j = threadIdx.x; j < n; j += kSmallMgsThreads) {
+      double wj = w[j];
+      if (i > 0) {
+        wj = __dsub_rn(wj, __dmul_rn(c, Vp[j]));
+        w[j] = wj;
+      }
+      acc = fma(wj, i <= k ? Vi[j] : wj, acc);
+    }
+    double h = block_sum_bcast(acc, red);
+    if (i == k + 1) h = sqrt(h);
+    if (threadIdx.x == 0) hcol[i] = h;
+    c = h;
+    Vp = Vi;
+  }
+  if (!(c > 1e-300)) return;
+  for (int64_t j = threadIdx.x; j < n; j += kSmallMgsThreads) vnext[j] = w[j] / c;
+}
+
 // V[k+1] = w / h if h > 1e-300 (else left zero: breakdown)
 __global__ void normalize_kernel(int64_t n, const double* __restrict__ w,
                                  const double* __restrict__ h, double* __restrict__ out) {
@@ -214,6 +266,16 @@ int gmres_core(cudaStream_t st, Krylov* K, int64_t n, const OpFn& A, const OpFn&
 // and the new Hessenberg column copied to the pinned host buffer.
 int enqueue_mgs(cudaStream_t st, Krylov* K, int64_t n, int k) {
   double* V = K->V.p;
+  const bool multi = g_comm_sys && (g_comm_sys->nranks > 1 || g_comm_sys->nccl);
+  const char* sv = getenv("MEHDG_MGS_SMALL");
+  if (!multi && n <= kSmallMgsN && !(sv && sv[0] == '0')) {
+    mgs_small_kernel<<<1, kSmallMgsThreads, 0, st>>>(n, K->w.p, V, k, K->hcol.p,
+                                                     V + (size_t)(k + 1) * n);
+    MH_CHECK_CUDA(cudaGetLastError());
+    MH_CHECK_CUDA(cudaMemcpyAsync(K->h_host, K->hcol.p, sizeof(double) * (k + 2),
+                                  cudaMemcpyDeviceToHost, st));
+    return MH_OK;
+  }
   for (int i = 0; i <= k; ++i) {
     const double* Vi = V + (size_t)i * n;
     const double* Vp = i > 0 ? V + (size_t)(i - 1) * n : nullptr;
