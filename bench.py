@@ -268,7 +268,7 @@ def run_reference(args, world, rank):
     prob = _REF_PROB
     cores = max(1, len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity")
                 else (os.cpu_count() or 1))
-    per = max(1, args.cpu_sample // 4)  # macros per core
+    per = max(1, args.ref_chunk)  # macros per core
     jobs = [(c * per, per, args.warmup, args.steps) for c in range(cores)
             if c * per < prob["N"]]
     with mp.get_context("fork").Pool(len(jobs)) as pool:
@@ -611,8 +611,12 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-sample", type=int, default=2048)
-    ap.add_argument("--cpu-reps", type=int, default=3)
+    # cpu_baseline leg of our arm: ~10 s of single-core oracle work at c2
+    # (factorisation of the sample + the timed applies)
+    ap.add_argument("--cpu-sample", type=int, default=16384)
+    ap.add_argument("--cpu-reps", type=int, default=5)
+    ap.add_argument("--ref-chunk", type=int, default=512,
+                    help="--impl reference: macros per host process per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-mb", action="store_true", help="skip the matrix-based mode timing")
     ap.add_argument("--profile-every", type=int, default=10,

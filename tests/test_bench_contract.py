@@ -31,7 +31,7 @@ COMMON = ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
 
 def test_reference_arm_contract():
     d = _run(["--impl", "reference", "--config", "c1", "--steps", "2", "--warmup", "3",
-              "--cpu-sample", "64"])
+              "--ref-chunk", "16"])
     for k in COMMON:
         assert k in d, k
     assert d["impl"] == "reference" and d["value"] > 0 and d["n_gpus"] == 1
