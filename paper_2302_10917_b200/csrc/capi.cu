@@ -544,12 +544,13 @@ static int apply_elements(mh_system* s, const double* u) {
     MH_CHECK_CUDA(cudaEventCreateWithFlags(&s->ev_int, cudaEventDisableTiming));
   }
   // everything earlier on the system stream (u, and the previous apply's use of
-  // V) precedes the interior macros
+  // V) precedes the interior macros; the exchange is enqueued first so that its
+  // NCCL kernel is resident before the persistent element grid fills the SMs
   MH_CHECK_CUDA(cudaEventRecord(s->ev_u, s->stream));
+  MH_CHECK(halo_u_exchange(s, u, nullptr));
   MH_CHECK_CUDA(cudaStreamWaitEvent(s->kstream, s->ev_u, 0));
   MH_CHECK(launch_element_range(s, kApply, u, s->V.p, s->kstream, split, s->N));
   MH_CHECK_CUDA(cudaEventRecord(s->ev_int, s->kstream));
-  MH_CHECK(halo_u_exchange(s, u, nullptr));
   MH_CHECK(launch_element_range(s, kApply, u, s->V.p, s->stream, 0, split));
   MH_CHECK_CUDA(cudaStreamWaitEvent(s->stream, s->ev_int, 0));
   return MH_OK;
