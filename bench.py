@@ -18,8 +18,9 @@ time, CUDA events on the library's stream, max over ranks), plus
   solve         GMRES(100) + D^-1 to 1e-10: iterations and seconds
   cpu_baseline  the CPU oracle (restatement of the reference algorithm) timed
                 on a bounded sample of the same workload on this host.
-`--impl reference` times that CPU restatement alone (the reference is pure
-Python and cannot be installed on the GPU box).
+`--impl reference` times the UNMODIFIED reference (`mehdg`, installed offline
+into baseline/_ref) on the host cores: condense + apply_schur at workers=1 and
+workers=cpu_count (baseline/reference_arm.py; never imports this package).
 """
 
 from __future__ import annotations
@@ -229,71 +230,18 @@ def config_block(name, prob, world, slabs=False):
             "parallelism": f"slabs{world} (NCCL halo)" if (world > 1 or slabs) else "single"}
 
 
-_REF_PROB = None  # the workload, inherited by the forked reference workers
-
-
-def _reference_worker(job):
-    """One host core: the oracle over its contiguous macro chunk, factorised, then
-    `steps` timed applies (BLAS single-threaded; the chunks run in parallel)."""
-    first, count, warmup, steps = job
-    from threadpoolctl import threadpool_limits
-
-    with threadpool_limits(limits=1):
-        o, ns, fs = oracle_sample(_REF_PROB, count, first=first)
-        o.factorize()
-        u = np.random.default_rng(1 + first).standard_normal(o.zhat)
-        for _ in range(warmup):
-            o.apply(u)
-        times = []
-        for _ in range(steps):
-            t0 = time.perf_counter()
-            o.apply(u)
-            times.append(time.perf_counter() - t0)
-    return ns, fs, times
-
-
 def run_reference(args, world, rank):
-    """--impl reference: the CPU restatement of the reference algorithm
-    (per-macro LAPACK loop as schur_solver.apply_schur), one process per host
-    core over contiguous macro chunks of a bounded sample of the workload."""
-    global _REF_PROB
+    """--impl reference: the unmodified reference solver (baseline/_ref) on the
+    host cores, same config / metric (baseline/reference_arm.py).  Under
+    torchrun only rank 0 runs it."""
     if rank != 0:
         return 0
-    import multiprocessing as mp
+    sys.path.insert(0, str(ROOT / "baseline"))
+    import reference_arm
 
-    from paper_2302_10917_b200 import synthetic as S
-
-    d, n, m, p = S.CONFIGS[args.config]
-    _REF_PROB = S.make_problem(d, n, m, p, seed=args.seed)
-    prob = _REF_PROB
-    cores = max(1, len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity")
-                else (os.cpu_count() or 1))
-    per = max(1, args.ref_chunk)  # macros per core
-    jobs = [(c * per, per, args.warmup, args.steps) for c in range(cores)
-            if c * per < prob["N"]]
-    with mp.get_context("fork").Pool(len(jobs)) as pool:
-        res = pool.map(_reference_worker, jobs)
-    ns = sum(r[0] for r in res)
-    fs = sum(r[1] for r in res)
-    # the chunks run concurrently: one step of the sample lasts as long as its slowest core
-    step_s = np.max(np.array([r[2] for r in res]), axis=0)
-    scale = prob["N"] / ns
-    ms = float(np.mean(step_s)) * scale * 1e3
-    value = 1e3 / ms
-    sample = (f"oracle port (per-macro scipy LAPACK loop as schur_solver.apply_schur), "
-              f"{len(jobs)} processes x {per} macros = macros [0,{ns}) of {prob['N']} and "
-              f"their {fs} faces; per-step time (max over processes) x{scale:.1f}")
-    line = {"impl": "reference", "metric": BASELINE_METRIC, "value": value, "unit": UNIT,
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded BASELINE generator)",
-            "config": config_block(args.config, prob, 1),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": len(jobs), "kind": "port",
-                             "sample": sample},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
-    print(json.dumps(line))
-    return 0
+    d, n, m, p = reference_arm._load_gen().CONFIGS[args.config]
+    return reference_arm.run(args.config, d, n, m, p, args.seed, args.steps, args.warmup,
+                             budget_s=args.ref_budget)
 
 
 def build_local(args, world, rank, dev):
@@ -615,8 +563,8 @@ def main():
     # (factorisation of the sample + the timed applies)
     ap.add_argument("--cpu-sample", type=int, default=16384)
     ap.add_argument("--cpu-reps", type=int, default=5)
-    ap.add_argument("--ref-chunk", type=int, default=512,
-                    help="--impl reference: macros per host process per step")
+    ap.add_argument("--ref-budget", type=float, default=150.0,
+                    help="--impl reference: seconds of timed applies per worker setting")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-mb", action="store_true", help="skip the matrix-based mode timing")
     ap.add_argument("--profile-every", type=int, default=10,

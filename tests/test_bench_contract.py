@@ -30,15 +30,18 @@ COMMON = ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
 
 
 def test_reference_arm_contract():
-    d = _run(["--impl", "reference", "--config", "c1", "--steps", "2", "--warmup", "3",
-              "--ref-chunk", "16"])
+    if not (ROOT / "baseline" / "_ref" / "mehdg").is_dir():
+        pytest.skip("reference not installed into baseline/_ref (__graft_entry__.build())")
+    d = _run(["--impl", "reference", "--config", "c1", "--steps", "2", "--warmup", "3"])
     for k in COMMON:
         assert k in d, k
     assert d["impl"] == "reference" and d["value"] > 0 and d["n_gpus"] == 1
     assert d["steps"] == 2 and d["warmup"] == 3 and d["higher_is_better"] is True
     assert "workload" in d["config"]
     cb = d["cpu_baseline"]
-    assert cb["value"] == d["value"] and cb["kind"] in ("port", "reference") and cb["cores"] >= 1
+    assert cb["value"] == d["value"] and cb["kind"] == "reference" and cb["cores"] >= 1
+    # the arm runs the unmodified reference and never loads this package
+    assert d["product_loaded"] is False and cb["extrapolated"] is False
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}
 
