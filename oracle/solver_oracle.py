@@ -328,3 +328,35 @@ def system_from_problem(prob) -> OracleSystem:
     return OracleSystem(prob["A"], prob["B"], prob["C"], prob["R_u"], prob["D"],
                         prob["R_hat"], prob["elem_face"], prob["face_elem"],
                         prob["face_slot"], prob["t"])
+
+
+def slab_system(prob, e0: int, e1: int):
+    """The oracle over the contiguous macro range [e0, e1) of a full-size problem
+    (a mesh slab: SURVEY 8(e) partitions by contiguous macro ids).
+
+    Keeps every unknown face touching a macro of the range, so each macro gathers
+    its whole uhat; sides outside the range are dropped.  Returns
+    ``(system, fidx, complete)``: ``fidx`` are the kept faces' global unknown-face
+    ids and ``complete`` marks the faces all of whose sides lie in the range -- on
+    those the slab's apply / RHS equal the whole mesh's (schur_solver.py:284-290,
+    247-253 sum the sides of a face only)."""
+    fe = np.asarray(prob["face_elem"], dtype=np.int64)
+    fs = np.asarray(prob["face_slot"], dtype=np.int64)
+
+    def inside(e):
+        return (e >= e0) & (e < e1)
+
+    touch = inside(fe[:, 0]) | inside(fe[:, 1])
+    fidx = np.nonzero(touch)[0]
+    remap = -np.ones(fe.shape[0], np.int64)
+    remap[fidx] = np.arange(fidx.size)
+    ef = np.asarray(prob["elem_face"][e0:e1], dtype=np.int64)
+    ef = np.where(ef >= 0, remap[np.maximum(ef, 0)], -1)
+    fe_s, fs_s = fe[fidx].copy(), fs[fidx].copy()
+    out = ~inside(fe_s)
+    fe_s[out], fs_s[out] = -1, -1
+    fe_s[~out] -= e0
+    complete = ~out[:, 0] & (~out[:, 1] | (fe[fidx, 1] < 0))
+    o = OracleSystem(prob["A"][e0:e1], prob["B"][e0:e1], prob["C"][e0:e1], prob["R_u"][e0:e1],
+                     prob["D"][fidx], prob["R_hat"][fidx], ef, fe_s, fs_s, prob["t"])
+    return o, fidx, complete

@@ -51,11 +51,20 @@ def gen_macros(N: int, Q: int, nc: int, seed: int = 0, first: int = 0, count: in
     def work(c):
         lo, hi = c * CHUNK, min((c + 1) * CHUNK, N)
         rng = np.random.default_rng([seed, 0, c])
+        s0, s1 = max(lo, first), min(hi, first + count)
+        if s0 == lo and s1 == hi:
+            # whole chunk in range: draw straight into the outputs (the same
+            # C-order stream as the temporary-array form below, no copies)
+            a = A[s0 - first:s1 - first]
+            rng.standard_normal(out=a)
+            a[:, np.arange(Q), np.arange(Q)] += Q
+            rng.standard_normal(out=Be[s0 - first:s1 - first])
+            rng.standard_normal(out=Ru[s0 - first:s1 - first])
+            return
         a = rng.standard_normal((hi - lo, Q, Q))
         a[:, np.arange(Q), np.arange(Q)] += Q
         b = rng.standard_normal((hi - lo, nc, Q))
         r = rng.standard_normal((hi - lo, Q))
-        s0, s1 = max(lo, first), min(hi, first + count)
         if s1 > s0:
             A[s0 - first:s1 - first] = a[s0 - lo:s1 - lo]
             Be[s0 - first:s1 - first] = b[s0 - lo:s1 - lo]

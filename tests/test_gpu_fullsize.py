@@ -1,0 +1,96 @@
+"""BASELINE c4 (d=3 n=24 m=3 p=3: N = 82,944, Q = 220) and c5 at n = 20 (N = 48,000,
+Q = 165) at FULL size on the device, checked against the CPU oracle on contiguous
+mesh slabs (the first x-slab, a middle one and the last one, so the highest macro
+and face ids -- 64-bit stream offsets, the last chunk of every stream -- are
+covered):
+
+* the reduced RHS f and the apply w = S uhat on every unknown face whose sides all
+  lie in the slab (schur_solver.py:243-253, 267-293): <= 1e-12 relative;
+* D^-1 w on every face the slab touches (schur_solver.py:296-305): <= 1e-12;
+* reconstruct_interior on the slab's macros, from the device solution
+  (schur_solver.py:423-431): <= 1e-9;
+* the GMRES solve (schur_solver.py:308-385): converged, its preconditioned
+  residual <= tol through the device operator, and the slab oracle's own
+  residual on the complete faces consistent with it;
+* bitwise determinism of a second apply at full size.
+
+The oracle is pinned to the reference at c1-c3 (tests/test_oracle_golden.py).
+Host memory: c4 holds ~70 GB of blocks; the test skips on smaller hosts.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import rel
+from oracle import solver_oracle as SO
+import paper_2302_10917_b200 as P
+from paper_2302_10917_b200 import synthetic as S
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+APPLY_TOL = 1e-12
+SOLVE_TOL = 1e-9
+
+
+def _segments(idx, t):
+    return (np.asarray(idx, np.int64)[:, None] * t + np.arange(t)).ravel()
+
+
+def _host_bytes_needed(name):
+    d, n, m, p = S.CONFIGS[name]
+    Q, t, nc = S.block_sizes(d, m, p)
+    N = 2 * n * n if d == 2 else 6 * n ** 3
+    return N * (Q * Q + nc * Q + Q) * 8 * 1.3
+
+
+@pytest.mark.parametrize("name", ["c5n20", "c4"])
+def test_full_size_against_oracle_slabs(gpu, name):
+    import psutil
+    import torch
+
+    need = _host_bytes_needed(name)
+    if psutil.virtual_memory().available < need:
+        pytest.skip(f"{name} needs ~{need / 1e9:.0f} GB of host memory")
+    prob = S.config_problem(name)
+    t, N, n = prob["t"], prob["N"], prob["n"]
+    cfg = P.SolverConfig(tol=1e-10)
+    tables = {"nfe": prob["d"] + 1, "elem_ufac": prob["elem_face"],
+              "face_elem": prob["face_elem"], "face_slot": prob["face_slot"],
+              "uidx": prob["uidx"], "F": prob["F"]}
+    sys_ = P.condense_arrays(prob["mesh"], prob["A"], None, prob["Be"], prob["R_u"], prob["D"],
+                             prob["R_hat"], cfg, tables=tables)
+    f = sys_.f_vec
+    uhat = prob["uhat"]
+    w = P.apply_schur(sys_, uhat)
+    assert np.array_equal(w, P.apply_schur(sys_, uhat))
+    z = P.apply_preconditioner(sys_, w)
+    x, info = P.gmres(P.SchurOperator(sys_), sys_.f_device, cfg, precond=P.Preconditioner(sys_))
+    assert info["converged"]
+    xh = x.cpu().numpy()
+    U = P.reconstruct_interior(sys_, x).cpu().numpy()
+    r = P.apply_preconditioner(sys_, f - P.apply_schur(sys_, xh))
+    Mf = np.linalg.norm(P.apply_preconditioner(sys_, f))
+    assert np.linalg.norm(r) <= 10 * cfg.tol * Mf
+    del x
+    torch.cuda.empty_cache()
+
+    slab = 6 * n * n  # one x-slab of Kuhn tets (mesh.py:407-417)
+    for e0 in (0, (n // 2) * slab, N - slab):
+        o, fidx, complete = SO.slab_system(prob, e0, e0 + slab)
+        o.factorize()
+        cseg = _segments(fidx[complete], t)
+        lseg = _segments(np.nonzero(complete)[0], t)
+        aseg = _segments(fidx, t)
+        assert complete.sum() > 0
+        assert rel(f[cseg], o.rhs()[lseg]) <= APPLY_TOL, f"{name} slab {e0}: rhs"
+        wo = o.apply(uhat[aseg])
+        assert rel(w[cseg], wo[lseg]) <= APPLY_TOL, f"{name} slab {e0}: apply"
+        assert rel(z[aseg], o.precond(w[aseg])) <= APPLY_TOL, f"{name} slab {e0}: D^-1"
+        Uo = o.reconstruct(xh[aseg])
+        assert rel(U[e0:e0 + slab], Uo) <= SOLVE_TOL, f"{name} slab {e0}: reconstruct"
+        # the oracle's residual of the device solution on the slab's complete faces
+        ro = o.precond(o.rhs() - o.apply(xh[aseg]))[lseg]
+        assert np.linalg.norm(ro) <= 10 * cfg.tol * Mf
+        assert rel(ro, r[cseg]) <= 1e-3 or np.linalg.norm(ro) <= 1e-3 * cfg.tol * Mf

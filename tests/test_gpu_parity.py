@@ -160,9 +160,10 @@ def _kind(k):
 
 
 @pytest.mark.parametrize("d,n,m,p", [(2, 4, 4, 3), (2, 3, 2, 5), (3, 2, 2, 3), (3, 2, 1, 4),
-                                     (3, 1, 3, 3), (2, 2, 3, 6)])
+                                     (3, 1, 3, 3), (2, 2, 3, 6), (3, 1, 2, 4), (3, 2, 2, 4)])
 def test_against_oracle_small(gpu, d, n, m, p):
-    """Each BASELINE block shape family (Q = 15..220) against the oracle."""
+    """Each BASELINE block shape family (Q = 15..220; c5's Q = 165, t = 45 on one and
+    on eight cubes) against the oracle, diagonally dominant as in BASELINE."""
     prob = S.make_problem(d, n, m, p, seed=7)
     sys_, cfg = condense_problem(prob)
     o = SO.system_from_problem(prob).factorize()

@@ -75,3 +75,27 @@ def test_slab_partition_properties(d, n, ranks):
     if slabs % ranks == 0:  # whole slabs, equal shares
         assert np.all(b % per == 0)
         assert len(set(np.diff(b).tolist())) == 1
+
+
+def test_slab_oracle_equals_whole_mesh_on_complete_faces():
+    """oracle.slab_system (the full-size GPU tests' checker): on faces whose sides
+    all lie in the slab, the slab's RHS / apply equal the whole mesh's."""
+    from oracle import solver_oracle as SO
+    from paper_2302_10917_b200 import synthetic as S
+
+    for d, n in ((2, 4), (3, 2)):
+        prob = S.make_problem(d, n, 1, 2, seed=3)
+        full = SO.system_from_problem(prob).factorize()
+        t = prob["t"]
+        wf, ff = full.apply(prob["uhat"]), full.rhs()
+        N = prob["N"]
+        for e0, e1 in ((0, N // 2), (N // 3, N), (N // 4, 3 * N // 4)):
+            o, fidx, complete = SO.slab_system(prob, e0, e1)
+            o.factorize()
+            seg = (fidx[:, None] * t + np.arange(t)).ravel()
+            ws = o.apply(prob["uhat"][seg]).reshape(-1, t)
+            assert complete.any() and not complete.all()
+            assert np.allclose(ws[complete], wf.reshape(-1, t)[fidx[complete]], rtol=0, atol=1e-12)
+            assert np.allclose(o.rhs().reshape(-1, t)[complete],
+                               ff.reshape(-1, t)[fidx[complete]], rtol=0, atol=1e-12)
+            assert not np.allclose(ws[~complete], wf.reshape(-1, t)[fidx[~complete]])
