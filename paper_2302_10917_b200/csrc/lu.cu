@@ -874,10 +874,15 @@ int launch_lu(mh_system* s, float* ms) {
   // MEHDG_LU=left|dmma|reg selects the earlier kernels for comparison
   const char* var = getenv("MEHDG_LU");
   const std::string choice = var ? std::string(var) : std::string();
-  const bool tile = (choice.empty() || choice == "tile") && Q > 32;
+  // the CTA-resident kernel (lu_cta.cu) measured slower than the warp-per-block
+  // tile kernel at every BASELINE shape: selectable, not the default
+  const bool cta = choice == "cta" && lu_cta_supported(Q);
+  const bool tile = !cta && (choice.empty() || choice == "tile" || choice == "cta") && Q > 32;
   const bool left = choice == "left" || (choice == "dmma" && Q > 96) || (choice == "reg" && Q > 128);
-  if (e0 && !tile) MH_CHECK_CUDA(cudaEventRecord(e0, s->stream));
-  if (tile) {
+  if (e0 && !tile && !cta) MH_CHECK_CUDA(cudaEventRecord(e0, s->stream));
+  if (cta) {
+    MH_CHECK(launch_lu_cta(s, g, e0));
+  } else if (tile) {
     MH_CHECK(launch_lu_tile(s, g, e0));  // records e0 after its scratch allocation
   } else if (left) {
     const unsigned gw = (unsigned)((s->N + kLeftWarps - 1) / kLeftWarps);

@@ -24,6 +24,8 @@ struct LuArgs {
 };
 
 int launch_lu_tile(mh_system* s, const LuArgs& g, cudaEvent_t start);
+int launch_lu_cta(mh_system* s, const LuArgs& g, cudaEvent_t start);
+bool lu_cta_supported(int Q);
 
 namespace {
 

@@ -58,3 +58,12 @@ def gpu():
 
     torch.cuda.init()
     return 0
+
+
+@pytest.fixture(params=["default", "cta"])
+def lu_kernel(request, monkeypatch):
+    """The default batched LU and the CTA-resident one (csrc/lu_cta.cu, 32 < Q <= 168),
+    chosen by MEHDG_LU when a system is factorized."""
+    if request.param == "cta":
+        monkeypatch.setenv("MEHDG_LU", "cta")
+    return request.param

@@ -161,7 +161,7 @@ def _kind(k):
 
 @pytest.mark.parametrize("d,n,m,p", [(2, 4, 4, 3), (2, 3, 2, 5), (3, 2, 2, 3), (3, 2, 1, 4),
                                      (3, 1, 3, 3), (2, 2, 3, 6), (3, 1, 2, 4), (3, 2, 2, 4)])
-def test_against_oracle_small(gpu, d, n, m, p):
+def test_against_oracle_small(gpu, d, n, m, p, lu_kernel):
     """Each BASELINE block shape family (Q = 15..220; c5's Q = 165, t = 45 on one and
     on eight cubes) against the oracle, diagonally dominant as in BASELINE."""
     prob = S.make_problem(d, n, m, p, seed=7)
@@ -201,7 +201,7 @@ def test_pivoting_blocks(gpu):
 @pytest.mark.parametrize("d,n,m,p", [(2, 2, 4, 2), (2, 2, 4, 3), (3, 1, 3, 2), (3, 1, 7, 1),
                                      (3, 1, 2, 4), (3, 1, 3, 3)])
 @pytest.mark.parametrize("kind", ["gauss", "ties"])
-def test_pivoting_blocks_tile_lu(gpu, d, n, m, p, kind):
+def test_pivoting_blocks_tile_lu(gpu, d, n, m, p, kind, lu_kernel):
     """Row interchanges in the tile LU (Q = 45, 91, 84, 120 (padded tile), 165, 220):
     LAPACK pivots bit-exact, including first-index ties (small-integer blocks)."""
     prob = S.make_problem(d, n, m, p, seed=13)
@@ -233,7 +233,7 @@ def test_singular_local_block_raises_with_id(gpu):
 
 
 @pytest.mark.parametrize("which", ["zero", "repeated_row"])
-def test_singular_local_block_tile_lu(gpu, which):
+def test_singular_local_block_tile_lu(gpu, which, lu_kernel):
     """Tile LU (Q = 91): the singular test min|U_jj| <= 1e-13 max|A| reports the first
     singular macro; a zero pivot skips the exchange and scaling (dgetf2 info > 0)."""
     prob = S.make_problem(2, 2, 4, 3, seed=3)
