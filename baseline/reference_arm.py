@@ -179,7 +179,7 @@ def product_loaded() -> bool:
         return False
 
 
-def run(config, d, n, m, p, seed, steps, warmup, budget_s=150.0, emit=print):
+def run(config, d, n, m, p, seed, steps, warmup, budget_s=150.0, emit=print, workers=None):
     if not (REF / "mehdg").is_dir():
         emit(json.dumps({"impl": "reference",
                          "unavailable": "baseline/_ref/mehdg missing (install the reference: "
@@ -214,7 +214,7 @@ def run(config, d, n, m, p, seed, steps, warmup, budget_s=150.0, emit=print):
     # apply) workers=1 runs all W + K applies
     scale = N_full / N
     results = {}
-    for workers in sorted({1, cores}):
+    for workers in (sorted({1, cores}) if workers is None else [workers]):
         sys_.pool = R.WorkerPool(workers)
         bud = budget_s if workers == 1 else budget_s / 2
         t0 = time.perf_counter()
@@ -266,3 +266,22 @@ def run(config, d, n, m, p, seed, steps, warmup, budget_s=150.0, emit=print):
         raise RuntimeError("reference arm loaded the product package")
     emit(json.dumps(line))
     return 0
+
+
+if __name__ == "__main__":
+    # python baseline/reference_arm.py CONFIG [--steps K] [--warmup W] [--workers N]
+    # (bench.py's cpu_baseline leg runs it in a separate process: the reference
+    # alone, workers=1, the whole workload)
+    import argparse
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("config")
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=1)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--workers", type=int, default=None)
+    ap.add_argument("--budget", type=float, default=60.0)
+    a = ap.parse_args()
+    d, n, m, p = _load_gen().CONFIGS[a.config]
+    sys.exit(run(a.config, d, n, m, p, a.seed, a.steps, a.warmup, budget_s=a.budget,
+                 workers=a.workers))

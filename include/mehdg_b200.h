@@ -137,6 +137,13 @@ int mh_refactorize_local(mh_system* sys, float* lu_ms);
 int mh_get_local_factors(mh_system* sys, int64_t first, int64_t count,
                          double* lu_host, int32_t* piv_host);
 
+/* The preconditioner's face inverses D_f^-1 (sign folded in) of the n
+ * unknown faces idx[], t x t row-major on the host.  The set form replaces
+ * them -- the drop-in honours a face factor replaced after condense
+ * (the reference's op.factor, schur_solver.py:137-154, 296-305). */
+int mh_get_face_inverse(mh_system* sys, int64_t n, const int32_t* idx, double* inv_host);
+int mh_set_face_inverse(mh_system* sys, int64_t n, const int32_t* idx, const double* inv_host);
+
 /* ---- the operator (device pointers, zhat doubles) -------------------- */
 
 /* f = R_hat - sum_e C A^-1 R_u   (condense reduced RHS, schur_solver.py:243-253) */

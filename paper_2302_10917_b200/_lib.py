@@ -82,6 +82,8 @@ SIGNATURES = {
     "mh_form_element_schur": [_p],
     "mh_apply_mb": [_p, _dp, _dp],
     "mh_get_element_schur": [_p, C.c_int64, C.c_int64, _dp],
+    "mh_get_face_inverse": [_p, C.c_int64, _p, _dp],
+    "mh_set_face_inverse": [_p, C.c_int64, _p, _dp],
     "mh_profile": [_p, C.c_int],
     "mh_profile_read": [_p, C.POINTER(C.c_double), _i64p, C.POINTER(C.c_double), _i64p],
     "mh_gmres": [_p, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int, _dp, _dp, _ip, _ip, _dp,

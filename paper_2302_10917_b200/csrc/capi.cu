@@ -5,7 +5,9 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <string>
 #include <thread>
 #include <vector>
@@ -104,6 +106,50 @@ static int need(mh_system* s, bool cond, const char* msg) {
   return MH_OK;
 }
 
+namespace mh {
+int launch_occupancy(int device, const void* kern, int threads, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> attr;           // smem attribute set
+  static std::map<std::tuple<int, const void*, int, size_t>, int> occ;  // resident CTAs / SM
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_tuple(device, kern, threads, smem);
+  auto it = occ.find(key);
+  if (it != occ.end()) return it->second;
+  size_t& cur = attr[{device, kern}];
+  if (smem > cur) {
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) {
+      set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+      return -1;
+    }
+    cur = smem;
+  }
+  int per_sm = 0;
+  const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+  if (e != cudaSuccess) {
+    set_error(std::string("cudaOccupancyMaxActiveBlocksPerMultiprocessor: ") + cudaGetErrorString(e));
+    return -1;
+  }
+  occ[key] = per_sm;
+  return per_sm;
+}
+
+void Knobs::read() {
+  auto env = [](const char* k) { return getenv(k); };
+  if (const char* v = env("MEHDG_LU")) lu = !strcmp(v, "tile") ? 1 : (!strcmp(v, "cta") ? 2 : 0);
+  if (const char* v = env("MEHDG_LU_CTAS")) lu_ctas = std::max(1, atoi(v));
+  if (const char* v = env("MEHDG_LU_SCR")) lu_scr_pol = atoi(v);
+  if (const char* v = env("MEHDG_LU_APOL")) lu_a_pol = atoi(v);
+  if (const char* v = env("MEHDG_ELEM_CTAS")) elem_ctas = std::max(0, atoi(v));
+  if (const char* v = env("MEHDG_ELEM_CH")) elem_ch = atoi(v);
+  if (const char* v = env("MEHDG_MGS_SMALL")) mgs_small = atoi(v);
+  if (const char* v = env("MEHDG_MGS_CTAS")) mgs_ctas = std::max(1, atoi(v));
+  if (const char* v = env("MEHDG_MGS_REG")) mgs_reg = atoi(v);
+  if (const char* v = env("MEHDG_GMRES_GRAPHS")) gmres_graphs = atoi(v);
+  if (const char* v = env("MEHDG_SPLIT_AT")) split_at = atoll(v);
+}
+}  // namespace mh
+
 extern "C" int mh_create(int device, int nfe, int64_t n_elem, int q, int t, int64_t n_face,
                          mh_system** out) {
   if (!out || nfe < 1 || nfe > kMaxSlots || n_elem < 0 || q < 1 || t < 1 || n_face < 0) {
@@ -117,6 +163,7 @@ extern "C" int mh_create(int device, int nfe, int64_t n_elem, int q, int t, int6
   *out = nullptr;
   MH_CHECK_CUDA(cudaSetDevice(device));
   mh_system* s = new mh_system();
+  s->knobs.read();
   s->device = device;
   s->nfe = nfe;
   s->N = n_elem;
@@ -142,7 +189,7 @@ extern "C" int mh_destroy(mh_system* s) {
   cudaSetDevice(s->device);
   if (s->stream) cudaStreamSynchronize(s->stream);
   s->elem_ufac.release(); s->face_vslot.release();
-  s->A.release(); s->LU.release(); s->lu_scr.release(); s->Lp.release(); s->Up.release(); s->udiag.release();
+  s->A.release(); s->lu_scr.release(); s->Lp.release(); s->Up.release(); s->udiag.release();
   s->dinv.release(); s->piv.release(); s->perm.release();
   s->lstat.release(); s->Bt.release(); s->Cm.release(); s->Ru.release(); s->D.release();
   s->Draw.release(); s->Rhat.release(); s->Dinv.release(); s->Fkind.release(); s->V.release();
@@ -482,6 +529,52 @@ extern "C" int mh_refactorize_local(mh_system* s, float* lu_ms) {
   return launch_lu(s, lu_ms);
 }
 
+// The explicit face inverses the preconditioner applies (sign folded in):
+// n faces (unknown-face indices idx[]), t x t row-major on the host.  The
+// device keeps them column-major (face.cu).
+static int face_inverse_io(mh_system* s, int64_t n, const int32_t* idx, double* host, bool set) {
+  MH_CHECK(need(s, s && s->factored, "face inverses before mh_factorize"));
+  if (n < 0 || (n && (!idx || !host))) {
+    set_error("mh_{get,set}_face_inverse: bad arguments");
+    return MH_E_ARG;
+  }
+  MH_CHECK_CUDA(cudaSetDevice(s->device));
+  const int t = s->t;
+  const size_t TT = (size_t)t * t;
+  std::vector<double> cm(TT);
+  for (int64_t k = 0; k < n; ++k) {
+    const int64_t f = idx[k];
+    if (f < 0 || f >= s->F) {
+      set_error("mh_{get,set}_face_inverse: face index out of range");
+      return MH_E_ARG;
+    }
+    double* hb = host + k * TT;
+    if (set) {
+      for (int i = 0; i < t; ++i)
+        for (int j = 0; j < t; ++j) cm[(size_t)j * t + i] = hb[(size_t)i * t + j];
+      MH_CHECK_CUDA(cudaMemcpyAsync(s->Dinv.p + f * TT, cm.data(), sizeof(double) * TT,
+                                    cudaMemcpyHostToDevice, s->stream));
+      MH_CHECK_CUDA(cudaStreamSynchronize(s->stream));
+    } else {
+      MH_CHECK_CUDA(cudaMemcpyAsync(cm.data(), s->Dinv.p + f * TT, sizeof(double) * TT,
+                                    cudaMemcpyDeviceToHost, s->stream));
+      MH_CHECK_CUDA(cudaStreamSynchronize(s->stream));
+      for (int i = 0; i < t; ++i)
+        for (int j = 0; j < t; ++j) hb[(size_t)i * t + j] = cm[(size_t)j * t + i];
+    }
+  }
+  return MH_OK;
+}
+
+extern "C" int mh_get_face_inverse(mh_system* s, int64_t n, const int32_t* idx, double* inv_host) {
+  return face_inverse_io(s, n, idx, inv_host, false);
+}
+
+extern "C" int mh_set_face_inverse(mh_system* s, int64_t n, const int32_t* idx,
+                                   const double* inv_host) {
+  return face_inverse_io(s, n, idx, const_cast<double*>(inv_host), true);
+}
+
 extern "C" int mh_get_local_factors(mh_system* s, int64_t first, int64_t count, double* lu_host,
                                     int32_t* piv_host) {
   MH_CHECK(need(s, s && s->factored, "factors requested before mh_factorize"));
@@ -530,10 +623,12 @@ extern "C" int mh_rhs(mh_system* s, double* f) {
 // run on a second stream while the halo exchange is in flight on the system
 // stream; the macros [0, e_split) follow the exchange (overlap the
 // interior-macro work with the halo).  Each macro's arithmetic is unchanged, so
-// the result is bitwise the same.  MEHDG_SPLIT_AT=k forces e_split = k (tests).
+// the result is bitwise the same.  MEHDG_SPLIT_AT=k moves the split to k (tests),
+// clamped to [e_split, N]: a smaller split would let halo-reading macros run
+// before the exchange.
 static int apply_elements(mh_system* s, const double* u) {
   int64_t split = s->e_split;
-  if (const char* v = getenv("MEHDG_SPLIT_AT")) split = std::min<int64_t>(s->N, atoll(v));
+  if (s->knobs.split_at >= 0) split = std::min<int64_t>(s->N, std::max<int64_t>(s->e_split, s->knobs.split_at));
   if (!multi_rank(s) || split >= s->N) {
     MH_CHECK(halo_u_exchange(s, u, nullptr));
     return launch_element(s, kApply, u, s->V.p);

@@ -75,6 +75,7 @@ struct ElemArgs {
   int64_t e_lo;  // macros [e_lo, N) are processed
   int Q, nc, t, nfe;
   int c_is_bt;
+  const int* skip;  // a stopped speculative GMRES step: return at once
 };
 
 // 8 per-lane partial sums -> the full sum of partial (lane >> 2) & 7, held by
@@ -182,6 +183,7 @@ __device__ __forceinline__ double dot_row(const double (&y)[R], const double* ri
 template <int R, int MODE, int RING, int CH>
 __global__ void __launch_bounds__(kThreads, MH_ELEM_MINB)
 element_kernel(ElemArgs a) {
+  if (a.skip && *a.skip) return;
   constexpr int S = RING / CH;
   using PipeT = Pipe<RING, CH, kWPB>;
   using ConsT = Consumer<RING, CH>;
@@ -461,23 +463,13 @@ int launch_rc(mh_system* s, const ElemArgs& a, cudaStream_t st) {
   // attribute + occupancy are host-side driver calls (microseconds): once per
   // instantiation and shared-memory size, not per apply (GMRES launches an
   // apply per Arnoldi step right after a host round trip)
-  struct Occ {
-    int dev = -1;
-    size_t smem = 0;
-    int per_sm = 0;
-  };
-  static thread_local Occ occ;
-  if (occ.dev != s->device || occ.smem != smem) {
-    MH_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 0;
-    MH_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
-    occ.dev = s->device;
-    occ.smem = smem;
-    occ.per_sm = per_sm;
-  }
-  int per_sm = occ.per_sm;
+  // the max-dynamic-smem attribute is per function and process-wide: a
+  // process-wide cache keyed by (device, kernel, smem), the attribute only ever
+  // raised (a launch with less smem stays valid), under a mutex
+  int per_sm = launch_occupancy(s->device, reinterpret_cast<const void*>(kern), kThreads, smem);
+  if (per_sm < 0) return MH_E_CUDA;
   if (per_sm < 1) per_sm = 1;
-  if (const char* v = getenv("MEHDG_ELEM_CTAS")) per_sm = std::max(1, std::min(per_sm, atoi(v)));
+  if (s->knobs.elem_ctas > 0) per_sm = std::max(1, std::min(per_sm, s->knobs.elem_ctas));
   int64_t grid = (int64_t)s->num_sms * per_sm;
   const int64_t need = (a.N - a.e_lo + kWPB - 1) / kWPB;
   if (grid > need) grid = need;
@@ -492,8 +484,7 @@ int launch_rm(mh_system* s, const ElemArgs& a, cudaStream_t st) {
   // alternatives at c2: 8 KB rings of 2 KB chunks at 16 consumers/SM -13%,
   // 12 KB rings of three 4 KB chunks -1.5%, 2 KB / 1 KB chunks (MEHDG_ELEM_CH)
   // -22% / -57%.
-  const char* cv = getenv("MEHDG_ELEM_CH");
-  const int ch = cv ? atoi(cv) : 512;
+  const int ch = s->knobs.elem_ch;
   if (ch == 256) return launch_rc<R, MODE, MH_ELEM_RING, 256>(s, a, st);
   if (ch == 128) return launch_rc<R, MODE, MH_ELEM_RING, 128>(s, a, st);
   return launch_rc<R, MODE, MH_ELEM_RING, 512>(s, a, st);
@@ -525,6 +516,7 @@ int launch_mode(mh_system* s, const double* uhat, double* out, cudaStream_t st, 
   a.t = s->t;
   a.nfe = s->nfe;
   a.c_is_bt = s->c_is_bt ? 1 : 0;
+  a.skip = MODE == kApply ? s->skip : nullptr;
   switch ((s->Q + 31) / 32) {
     case 1: return launch_rm<1, MODE>(s, a, st);
     case 2: return launch_rm<2, MODE>(s, a, st);

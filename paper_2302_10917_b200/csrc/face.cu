@@ -37,6 +37,7 @@ struct FaceArgs {
   const double* Dinv;
   int64_t F;
   int t;
+  const int* skip;  // a stopped speculative GMRES step: return at once
 };
 
 // z <- M z for the column-major t x t matrix M (rows lane + 32 r); the input
@@ -64,6 +65,7 @@ __device__ __forceinline__ void warp_gemv(double (&z)[RT], const double* __restr
 
 template <int RT, bool RHS, bool PRE>
 __global__ void __launch_bounds__(kFaceWarps * 32) face_reduce_kernel(FaceArgs a) {
+  if (a.skip && *a.skip) return;
   extern __shared__ double s_buf[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t f = (int64_t)blockIdx.x * kFaceWarps + w;
@@ -121,6 +123,7 @@ __global__ void __launch_bounds__(kFaceWarps * 32) face_reduce_kernel(FaceArgs a
 // front (static unroll over TMAX = G columns) for memory-level parallelism.
 template <int G, bool RHS, bool PRE>
 __global__ void __launch_bounds__(kFaceWarps * 32) face_small_kernel(FaceArgs a) {
+  if (a.skip && *a.skip) return;
   __shared__ double s_u[kFaceWarps * 32];
   constexpr int FPB = kFaceWarps * 32 / G;  // faces per CTA
   const int tid = threadIdx.x, g = tid % G, grp = tid / G;
@@ -180,6 +183,7 @@ __global__ void __launch_bounds__(kFaceWarps * 32) face_small_kernel(FaceArgs a)
 
 template <int RT>
 __global__ void __launch_bounds__(kFaceWarps * 32) precond_kernel(FaceArgs a) {
+  if (a.skip && *a.skip) return;
   extern __shared__ double s_buf[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t f = (int64_t)blockIdx.x * kFaceWarps + w;
@@ -389,6 +393,7 @@ FaceArgs make_args(mh_system* s, const double* in, double* out) {
   a.uhat = in;
   a.out = out;
   a.Dinv = s->Dinv.p;
+  a.skip = s->skip;
   a.F = s->F;
   a.t = s->t;
   return a;

@@ -12,20 +12,42 @@
 // and the cycle-end triangular solve run on the host in double, exactly
 // as the reference does them in numpy.
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <vector>
 
 #include "mh_internal.h"
 
 namespace mh {
 
+constexpr int kDotPartsMax = 2048;  // partials of a dot product (one warp each)
+constexpr int kDotWarps = 8;        // warps per block of the grid dot kernel
+
+// The number of partials of an n-vector dot product: a power of two near n / 64
+// in [32, 2048] (a few elements per lane: each reduction phase is one memory
+// round trip) -- a function of n alone, so every kernel (and rank count) that
+// reduces the same vector uses the same partition.
+__host__ __device__ inline int dot_parts(int64_t n) {
+  int p = 32;
+  while (p < kDotPartsMax && (int64_t)p * 2 * 64 <= n) p *= 2;
+  return p;
+}
+
 struct Krylov {
   int64_t n = 0;
   int restart = 0;
   DBuf<double> V, w, tmp, tmp2, part, hcol, ydev, scal;
-  DBuf<unsigned> ticket;
+  DBuf<unsigned> ticket, bar;  // bar: the MGS kernel's grid barrier (count, generation)
+  int num_sms = 148;
   double* h_host = nullptr;  // pinned
+  // device Arnoldi pipeline (pipelined solves): the Hessenberg matrix, the
+  // rotations, g, the per-step residual estimates and the control block
+  DBuf<double> Hd, csd, snd, gd, histd;
+  DBuf<int> ctl;             // GmresCtl
+  int* ctl_host = nullptr;   // pinned, two slots of kCtlInts
+  const int* skip = nullptr; // &ctl->stop while a pipelined cycle runs
   bool persistent = false;   // a system's workspace, reused across solves
   // CUDA graphs of the Arnoldi step's MGS block, one per basis size k (captured
   // on first use, replayed afterwards; they bake in the buffer addresses above)
@@ -46,14 +68,28 @@ struct Krylov {
     MH_CHECK(w.alloc((size_t)n));
     MH_CHECK(tmp.alloc((size_t)n));
     MH_CHECK(tmp2.alloc((size_t)n));
-    MH_CHECK(part.alloc(kDotBlocks));
+    MH_CHECK(part.alloc(2 * kDotPartsMax));
     MH_CHECK(hcol.alloc((size_t)restart + 2));
+    MH_CHECK(bar.alloc(2));
+    MH_CHECK_CUDA(cudaMemset(bar.p, 0, 2 * sizeof(unsigned)));
+    {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
     MH_CHECK(ydev.alloc((size_t)restart + 1));
     MH_CHECK(scal.alloc(4));
     MH_CHECK(ticket.alloc(1));
     MH_CHECK_CUDA(cudaMemset(ticket.p, 0, sizeof(unsigned)));
     if (h_host) cudaFreeHost(h_host);
-    MH_CHECK_CUDA(cudaMallocHost(&h_host, sizeof(double) * (restart + 4)));
+    MH_CHECK_CUDA(cudaMallocHost(&h_host, sizeof(double) * ((size_t)(restart + 1) * restart + 4 * restart + 8)));
+    MH_CHECK(Hd.alloc((size_t)(restart + 1) * restart));
+    MH_CHECK(csd.alloc((size_t)restart));
+    MH_CHECK(snd.alloc((size_t)restart));
+    MH_CHECK(gd.alloc((size_t)restart + 1));
+    MH_CHECK(histd.alloc((size_t)restart));
+    MH_CHECK(ctl.alloc(8));
+    if (!ctl_host) MH_CHECK_CUDA(cudaMallocHost(&ctl_host, sizeof(int) * 16));
     return MH_OK;
   }
   ~Krylov() {
@@ -62,8 +98,10 @@ struct Krylov {
     if (ev_in) cudaEventDestroy(ev_in);
     if (ev_out) cudaEventDestroy(ev_out);
     V.release(); w.release(); tmp.release(); tmp2.release(); part.release();
-    hcol.release(); ydev.release(); scal.release(); ticket.release();
+    hcol.release(); ydev.release(); scal.release(); ticket.release(); bar.release();
+    Hd.release(); csd.release(); snd.release(); gd.release(); histd.release(); ctl.release();
     if (h_host) cudaFreeHost(h_host);
+    if (ctl_host) cudaFreeHost(ctl_host);
   }
 };
 
@@ -71,119 +109,306 @@ void free_krylov(Krylov* k) { delete k; }
 
 namespace {
 
-__device__ __forceinline__ double block_sum(double v, double* red) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+// ---- deterministic dot products --------------------------------------
+// A dot product is the fixed-order sum of P = dot_parts(n) partials; partial b
+// covers [n b / P, n (b+1) / P) and is computed by ONE warp (lane l
+// accumulates elements lo + l, lo + l + 32, ... with fma, then a fixed xor
+// tree).  The final sum: lane l adds partials l, l + 32, ... in order, then the
+// same xor tree.  The grid kernel (a warp per partial, last-block-done final
+// sum) and the one-CTA MGS kernel (each warp several partials) therefore give
+// bitwise the same value -- as do 1 and N ranks (rank partials all-gathered and
+// added in rank order).
+
+__device__ __forceinline__ double warp_xor_sum(double v) {
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  double r = 0.0;
-  if (threadIdx.x == 0)
-    for (int i = 0; i < kDotThreads / 32; ++i) r += red[i];
-  return r;  // valid on thread 0
+  return v;
+}
+
+// partial b of (w - c Vp) . y, updating w in place when coef is given
+// (mode 1: y = Vi; mode 2: y = w itself)
+__device__ __forceinline__ double dot_partial(int64_t n, int P, int b, double* __restrict__ w,
+                                              const double* __restrict__ Vp, double c, bool upd,
+                                              const double* __restrict__ Vi, int mode, int lane) {
+  const int64_t lo = n * b / P, hi = n * (b + 1) / P;
+  double acc = 0.0;
+  // batches of 8 elements per lane: all loads of a batch first (w may alias
+  // nothing, but the compiler cannot move loads above the previous stores)
+  for (int64_t i0 = lo + lane; i0 < hi; i0 += 32 * 8) {
+    double wv[8], pv[8], yv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t i = i0 + 32 * u;
+      const bool ok = i < hi;
+      wv[u] = ok ? w[i] : 0.0;
+      pv[u] = (ok && upd) ? Vp[i] : 0.0;
+      yv[u] = (ok && mode != 2) ? Vi[i] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t i = i0 + 32 * u;
+      if (i < hi) {
+        double wi = wv[u];
+        if (upd) {
+          wi = __dsub_rn(wi, __dmul_rn(c, pv[u]));  // numpy: wv -= H*V (two roundings)
+          w[i] = wi;
+        }
+        acc = fma(wi, mode == 2 ? wi : yv[u], acc);
+      }
+    }
+  }
+  return warp_xor_sum(acc);
+}
+
+// the fixed-order sum of the P partials (one warp).  The partials were
+// published before a fence + barrier / ticket: L2-coherent loads (ld.cg, no
+// stale L1 line), issued together rather than one volatile load at a time
+__device__ __forceinline__ double parts_sum(const double* part, int P, int lane) {
+  double v = 0.0;
+#pragma unroll 8
+  for (int i = lane; i < P; i += 32) v += __ldcg(part + i);
+  return warp_xor_sum(v);
 }
 
 // Fused MGS step.  mode 0: plain dot(x, y); mode 1: w -= c*Vp then dot(Vi, w);
 // mode 2: w -= c*Vp then dot(w, w) and out <- sqrt.  Result to *out (device).
-__global__ void __launch_bounds__(kDotThreads)
+// A set *skip (a stopped speculative GMRES step) makes it a no-op.
+__global__ void __launch_bounds__(kDotWarps * 32)
 dot_kernel(int64_t n, double* __restrict__ w, const double* __restrict__ Vp,
            const double* __restrict__ coef, const double* __restrict__ Vi, int mode,
            bool take_sqrt, double* __restrict__ part, unsigned* __restrict__ ticket,
-           double* __restrict__ out) {
-  __shared__ double red[kDotThreads / 32];
+           double* __restrict__ out, const int* __restrict__ skip) {
+  if (skip && *skip) return;
   __shared__ bool last;
-  const int64_t b = blockIdx.x;
-  const int64_t lo = n * b / kDotBlocks, hi = n * (b + 1) / kDotBlocks;
-  const double c = (mode != 0 && coef) ? *coef : 0.0;
-  double acc = 0.0;
-  for (int64_t i = lo + threadIdx.x; i < hi; i += kDotThreads) {
-    double wi = w[i];
-    if (mode != 0 && coef) {
-      wi = __dsub_rn(wi, __dmul_rn(c, Vp[i]));  // numpy: wv -= H*V (two roundings)
-      w[i] = wi;
-    }
-    const double yi = (mode == 2) ? wi : Vi[i];
-    acc = fma(wi, yi, acc);
-  }
-  const double s = block_sum(acc, red);
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int b = blockIdx.x * kDotWarps + wp;
+  const int P = gridDim.x * kDotWarps;
+  const bool upd = mode != 0 && coef;
+  const double c = upd ? *coef : 0.0;
+  const double s = dot_partial(n, P, b, w, Vp, c, upd, Vi, mode, lane);
+  if (lane == 0) part[b] = s;
+  __syncthreads();
   if (threadIdx.x == 0) {
-    part[b] = s;
     __threadfence();
     const unsigned tk = atomicAdd(ticket, 1u);
-    last = (tk == kDotBlocks - 1);
+    last = (tk == gridDim.x - 1);
   }
   __syncthreads();
-  if (!last) return;
+  if (!last || wp != 0) return;
   __threadfence();
-  // fixed-order final reduction of the 512 partials
-  double v = 0.0;
-  for (int i = threadIdx.x; i < kDotBlocks; i += kDotThreads) v += ((volatile double*)part)[i];
-  const double tot = block_sum(v, red);
-  if (threadIdx.x == 0) {
+  const double tot = parts_sum(part, P, lane);
+  if (lane == 0) {
     *out = (mode == 2 && take_sqrt) ? sqrt(tot) : tot;
     *ticket = 0u;
   }
 }
 
-// The whole MGS block of Arnoldi step k in ONE CTA for short vectors (n <=
-// kSmallMgsN): the k + 2 dependent reductions are block reductions instead of
-// k + 2 grid launches (launch latency bounds them at this size).  Same
-// arithmetic per element as dot_kernel (w -= h V in two roundings, fma dots);
-// each thread owns the same indices in every pass, so the in-place updates
-// need no synchronisation beyond the reductions.
-constexpr int kSmallMgsThreads = 1024;
-constexpr int64_t kSmallMgsN = 1 << 16;
+// The whole MGS block of Arnoldi step k in ONE launch: the k + 2 dependent
+// reductions (H[0..k, k] and ||w||), each followed by a grid-wide barrier,
+// then V[k+1] = w / ||w||.  Warp gw computes partials gw, gw + (all warps),
+// ... exactly as dot_kernel's warps do, every block then sums the same
+// partials in the same order (double-buffered, so one barrier per reduction):
+// the results are bitwise those of k + 2 dot_kernel launches.  8-warp CTAs
+// (MEHDG_MGS_CTAS per SM at most), launched cooperatively (all resident).
+constexpr int kMgsThreads = 256;
 
-__device__ __forceinline__ double block_sum_bcast(double v, double* red) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-  if (lane == 0) red[warp] = v;
+
+__device__ __forceinline__ void grid_barrier(unsigned* count, volatile unsigned* gen) {
   __syncthreads();
-  if (warp == 0) {
-    double r = lane < kSmallMgsThreads / 32 ? red[lane] : 0.0;
-    for (int o = 16; o; o >>= 1) r += __shfl_xor_sync(kFull, r, o);
-    if (lane == 0) red[32] = r;
+  if (threadIdx.x == 0) {
+    const unsigned g0 = *gen;
+    __threadfence();
+    if (atomicAdd(count, 1u) == gridDim.x - 1) {
+      *count = 0u;
+      __threadfence();
+      atomicAdd(const_cast<unsigned*>(gen), 1u);
+    } else {
+      while (*gen == g0) __nanosleep(64);  // back off: one L2 line polled by every CTA
+    }
+    __threadfence();
   }
   __syncthreads();
-  const double r = red[32];
-  __syncthreads();
-  return r;
 }
 
-__global__ void __launch_bounds__(kSmallMgsThreads)
-mgs_small_kernel(int64_t n, double* __restrict__ w, const double* __restrict__ V, int k,
-                 double* __restrict__ hcol, double* __restrict__ vnext) {
-  __shared__ double red[33];
+__global__ void __launch_bounds__(kMgsThreads)
+mgs_kernel(int64_t n, double* __restrict__ w, const double* __restrict__ V, int k,
+           double* __restrict__ hcol, double* __restrict__ vnext, double* __restrict__ part2,
+           unsigned* __restrict__ bar, const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  __shared__ double hs;
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int WB = kMgsThreads / 32;
+  const int gw = blockIdx.x * WB + wp, nw = gridDim.x * WB;
+  const int P = dot_parts(n);
   double c = 0.0;
   const double* Vp = nullptr;
   for (int i = 0; i <= k + 1; ++i) {
     const double* Vi = V + (size_t)i * n;  // i = k + 1: the norm of w
-    double acc = 0.0;
-    for (int64_t j = threadIdx.x; j < n; j += kSmallMgsThreads) {
-      double wj = w[j];
-      if (i > 0) {
-        wj = __dsub_rn(wj, __dmul_rn(c, Vp[j]));
-        w[j] = wj;
-      }
-      acc = fma(wj, i <= k ? Vi[j] : wj, acc);
+    const int mode = i <= k ? 1 : 2;
+    double* part = part2 + (i & 1) * kDotPartsMax;
+    for (int b = gw; b < P; b += nw) {
+      const double pv = dot_partial(n, P, b, w, Vp, c, i > 0, Vi, mode, lane);
+      if (lane == 0) part[b] = pv;
     }
-    double h = block_sum_bcast(acc, red);
-    if (i == k + 1) h = sqrt(h);
-    if (threadIdx.x == 0) hcol[i] = h;
-    c = h;
+    if (gridDim.x > 1) grid_barrier(bar, bar + 1);
+    else __syncthreads();
+    if (wp == 0) {
+      double h = parts_sum(part, P, lane);
+      if (i == k + 1) h = sqrt(h);
+      if (lane == 0) {
+        hs = h;
+        if (blockIdx.x == 0) hcol[i] = h;
+      }
+    }
+    __syncthreads();
+    c = hs;
     Vp = Vi;
   }
   if (!(c > 1e-300)) return;
-  for (int64_t j = threadIdx.x; j < n; j += kSmallMgsThreads) vnext[j] = w[j] / c;
+  for (int64_t j = blockIdx.x * (int64_t)kMgsThreads + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * kMgsThreads)
+    vnext[j] = w[j] / c;
+}
+
+// The same MGS block with w and the previous basis vector held in registers
+// (a warp per partial, at most E elements per lane): each reduction reads one
+// basis vector from memory and nothing is written until V[k+1] = w / ||w||.
+// Per element the operations and their order are dot_partial's, so the
+// results are bitwise those of mgs_kernel / dot_kernel.
+template <int E>
+__global__ void __launch_bounds__(kMgsThreads)
+mgs_reg_kernel(int64_t n, const double* __restrict__ w, const double* __restrict__ V, int k,
+               double* __restrict__ hcol, double* __restrict__ vnext,
+               double* __restrict__ part2, unsigned* __restrict__ bar,
+               const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  __shared__ double hs;
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int b = blockIdx.x * (kMgsThreads / 32) + wp;
+  const int P = dot_parts(n);
+  const int64_t lo = b < P ? n * b / P : 0, hi = b < P ? n * (b + 1) / P : 0;
+  double wr[E], vp[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int64_t j = lo + lane + 32 * e;
+    wr[e] = j < hi ? w[j] : 0.0;
+    vp[e] = 0.0;
+  }
+  double c = 0.0;
+  for (int i = 0; i <= k + 1; ++i) {
+    const double* Vi = V + (size_t)i * n;
+    double yv[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int64_t j = lo + lane + 32 * e;
+      yv[e] = (i <= k && j < hi) ? Vi[j] : 0.0;
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int64_t j = lo + lane + 32 * e;
+      if (j < hi) {
+        double wi = wr[e];
+        if (i > 0) wi = __dsub_rn(wi, __dmul_rn(c, vp[e]));
+        wr[e] = wi;
+        acc = fma(wi, i <= k ? yv[e] : wi, acc);
+      }
+      vp[e] = yv[e];
+    }
+    acc = warp_xor_sum(acc);
+    double* part = part2 + (i & 1) * kDotPartsMax;
+    if (lane == 0 && b < P) part[b] = acc;
+    grid_barrier(bar, bar + 1);
+    if (wp == 0) {
+      double h = parts_sum(part, P, lane);
+      if (i == k + 1) h = sqrt(h);
+      if (lane == 0) {
+        hs = h;
+        if (blockIdx.x == 0) hcol[i] = h;
+      }
+    }
+    __syncthreads();
+    c = hs;
+  }
+  if (!(c > 1e-300)) return;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int64_t j = lo + lane + 32 * e;
+    if (j < hi) vnext[j] = wr[e] / c;
+  }
 }
 
 // V[k+1] = w / h if h > 1e-300 (else left zero: breakdown)
 __global__ void normalize_kernel(int64_t n, const double* __restrict__ w,
-                                 const double* __restrict__ h, double* __restrict__ out) {
+                                 const double* __restrict__ h, double* __restrict__ out,
+                                 const int* __restrict__ skip) {
+  if (skip && *skip) return;
   const double hv = *h;
   if (!(hv > 1e-300)) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     out[i] = w[i] / hv;
+}
+
+// Control block of a pipelined GMRES cycle (device ints)
+enum GmresCtl { kStop = 0, kKUsed = 1, kIt = 2, kConv = 3, kBreak = 4, kSteps = 5 };
+constexpr int kCtlInts = 8;
+constexpr int kMaxRestartSmem = 1024;  // restart lengths the device Givens supports
+
+// Step k's Givens update on the device, the reference's arithmetic
+// (schur_solver.py:351-375): the new Hessenberg column, the previous rotations,
+// the new rotation, g, the residual estimate and the stopping rules.  Once a
+// cycle stops (converged, breakdown, maxiter) every later step of it is a no-op
+// -- the host enqueues steps ahead without waiting for each one.
+__global__ void givens_kernel(const double* __restrict__ hcol, double* __restrict__ H,
+                              double* __restrict__ cs, double* __restrict__ sn,
+                              double* __restrict__ g, double* __restrict__ hist,
+                              int* __restrict__ ctl, int k, int m, double bnorm, double tol,
+                              int maxiter) {
+  __shared__ double sh[kMaxRestartSmem + 2], sc[kMaxRestartSmem], ss[kMaxRestartSmem];
+  if (ctl[kStop]) return;
+  const int lane = threadIdx.x;
+  for (int i = lane; i <= k + 1; i += 32) sh[i] = hcol[i];
+  for (int i = lane; i < k; i += 32) {
+    sc[i] = cs[i];
+    ss[i] = sn[i];
+  }
+  __syncwarp();
+  if (lane == 0) {
+    const bool breakdown = !(sh[k + 1] > 1e-300);
+    for (int i = 0; i < k; ++i) {
+      const double tt = sc[i] * sh[i] + ss[i] * sh[i + 1];
+      sh[i + 1] = -ss[i] * sh[i] + sc[i] * sh[i + 1];
+      sh[i] = tt;
+    }
+    const double denom = hypot(sh[k], sh[k + 1]);
+    if (denom == 0.0) {
+      ctl[kKUsed] = k + 1;
+      ctl[kBreak] = 1;
+      ctl[kStop] = 1;
+    } else {
+      const double c = sh[k] / denom, sgn = sh[k + 1] / denom;
+      cs[k] = c;
+      sn[k] = sgn;
+      sh[k] = denom;
+      sh[k + 1] = 0.0;
+      const double gk = g[k];
+      g[k + 1] = -sgn * gk;
+      g[k] = c * gk;
+      const int it = ++ctl[kIt];
+      const double res = fabs(g[k + 1]);
+      hist[ctl[kSteps]++] = res;
+      ctl[kKUsed] = k + 1;
+      if (res / bnorm <= tol) {
+        ctl[kConv] = 1;
+        ctl[kStop] = 1;
+      } else if (breakdown || it >= maxiter) {
+        ctl[kBreak] = breakdown ? 1 : 0;
+        ctl[kStop] = 1;
+      }
+    }
+  }
+  __syncwarp();
+  for (int i = lane; i <= k + 1; i += 32) H[(size_t)i * m + k] = sh[i];
 }
 
 __global__ void scale_kernel(int64_t n, const double* __restrict__ x, double inv_div,
@@ -232,11 +457,23 @@ struct OpFn {
 // sum is all-gathered and added in rank order, identically on every rank.
 thread_local mh_system* g_comm_sys = nullptr;  // bound for the duration of one solve
 
+// the Krylov knobs also serve operator-only solves (mh_gmres_op, no system):
+// read once per process
+const Knobs& proc_knobs() {
+  static const Knobs k = [] {
+    Knobs x;
+    x.read();
+    return x;
+  }();
+  return k;
+}
+
 int dot_dev(cudaStream_t st, Krylov* K, int64_t n, double* w, const double* Vp,
             const double* coef, const double* Vi, int mode, double* out) {
   const bool multi = g_comm_sys && (g_comm_sys->nranks > 1 || g_comm_sys->nccl);
-  dot_kernel<<<kDotBlocks, kDotThreads, 0, st>>>(n, w, Vp, coef, Vi, mode, !multi, K->part.p,
-                                                  K->ticket.p, multi ? K->scal.p + 3 : out);
+  dot_kernel<<<dot_parts(n) / kDotWarps, kDotWarps * 32, 0, st>>>(
+      n, w, Vp, coef, Vi, mode, !multi, K->part.p, K->ticket.p, multi ? K->scal.p + 3 : out,
+      K->skip);
   MH_CHECK_CUDA(cudaGetLastError());
   if (multi) MH_CHECK(allreduce_scalar(g_comm_sys, K->scal.p + 3, out, mode == 2));
   return MH_OK;
@@ -264,16 +501,45 @@ int gmres_core(cudaStream_t st, Krylov* K, int64_t n, const OpFn& A, const OpFn&
 
 // The MGS block of Arnoldi step k: H[0..k, k] and H[k+1, k] = ||w||, V[k+1] = w / H[k+1, k],
 // and the new Hessenberg column copied to the pinned host buffer.
-int enqueue_mgs(cudaStream_t st, Krylov* K, int64_t n, int k) {
+int enqueue_mgs(cudaStream_t st, Krylov* K, int64_t n, int k, bool copy_host = true) {
   double* V = K->V.p;
   const bool multi = g_comm_sys && (g_comm_sys->nranks > 1 || g_comm_sys->nccl);
-  const char* sv = getenv("MEHDG_MGS_SMALL");
-  if (!multi && n <= kSmallMgsN && !(sv && sv[0] == '0')) {
-    mgs_small_kernel<<<1, kSmallMgsThreads, 0, st>>>(n, K->w.p, V, k, K->hcol.p,
-                                                     V + (size_t)(k + 1) * n);
-    MH_CHECK_CUDA(cudaGetLastError());
-    MH_CHECK_CUDA(cudaMemcpyAsync(K->h_host, K->hcol.p, sizeof(double) * (k + 2),
-                                  cudaMemcpyDeviceToHost, st));
+  if (!multi && proc_knobs().mgs_small) {
+    // one launch for the whole block: a warp per partial with w in registers
+    // when every partial fits E elements per lane and the grid, else memory
+    const int P = dot_parts(n);
+    const int64_t per_lane = (n / P + 1 + 31) / 32;
+    const int wpb = kMgsThreads / 32;
+    const void* fn = (const void*)mgs_kernel;
+    int G = std::max(1, std::min(K->num_sms * proc_knobs().mgs_ctas, P / wpb));
+    if (proc_knobs().mgs_reg && per_lane <= 16) {
+      const void* fr = per_lane <= 4 ? (const void*)mgs_reg_kernel<4>
+                       : per_lane <= 8 ? (const void*)mgs_reg_kernel<8>
+                                       : (const void*)mgs_reg_kernel<16>;
+      int dev = 0;
+      MH_CHECK_CUDA(cudaGetDevice(&dev));
+      const int per_sm = launch_occupancy(dev, fr, kMgsThreads, 0);
+      if (per_sm > 0 && P / wpb <= per_sm * K->num_sms) {  // all CTAs co-resident
+        G = P / wpb;
+        fn = fr;
+      }
+    }
+    double* vnext = V + (size_t)(k + 1) * n;
+    void* args[] = {(void*)&n, (void*)&K->w.p, (void*)&V, (void*)&k, (void*)&K->hcol.p,
+                    (void*)&vnext, (void*)&K->part.p, (void*)&K->bar.p, (void*)&K->skip};
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(G);
+    cfg.blockDim = dim3(kMgsThreads);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = G > 1 ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    MH_CHECK_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
+    if (copy_host)
+      MH_CHECK_CUDA(cudaMemcpyAsync(K->h_host, K->hcol.p, sizeof(double) * (k + 2),
+                                    cudaMemcpyDeviceToHost, st));
     return MH_OK;
   }
   for (int i = 0; i <= k; ++i) {
@@ -285,17 +551,19 @@ int enqueue_mgs(cudaStream_t st, Krylov* K, int64_t n, int k) {
   MH_CHECK(dot_dev(st, K, n, K->w.p, V + (size_t)k * n, K->hcol.p + k, nullptr, 2,
                    K->hcol.p + k + 1));
   normalize_kernel<<<dim3(1184), dim3(256), 0, st>>>(n, K->w.p, K->hcol.p + k + 1,
-                                                     V + (size_t)(k + 1) * n);
+                                                     V + (size_t)(k + 1) * n, K->skip);
   MH_CHECK_CUDA(cudaGetLastError());
-  MH_CHECK_CUDA(cudaMemcpyAsync(K->h_host, K->hcol.p, sizeof(double) * (k + 2),
-                                cudaMemcpyDeviceToHost, st));
+  if (copy_host)
+    MH_CHECK_CUDA(cudaMemcpyAsync(K->h_host, K->hcol.p, sizeof(double) * (k + 2),
+                                  cudaMemcpyDeviceToHost, st));
   return MH_OK;
 }
 
-// Replays (capturing on first use) the graph of step k on a private stream
-// ordered after `st`; returns with the Hessenberg column in K->h_host.  The
+// Replays (capturing on first use, on a private stream) the graph of step k's
+// MGS block in order on `st`; asynchronous.  The
 // k + 3 launches of a step then cost one graph launch: same kernels, same
-// arguments, bitwise the same results.
+// arguments, bitwise the same results.  Pipelined solves only (the graph
+// leaves the Hessenberg column on the device for givens_kernel).
 int run_mgs(cudaStream_t st, Krylov* K, int64_t n, int k) {
   if (!K->gs) {
     MH_CHECK_CUDA(cudaStreamCreateWithFlags(&K->gs, cudaStreamNonBlocking));
@@ -306,19 +574,14 @@ int run_mgs(cudaStream_t st, Krylov* K, int64_t n, int k) {
   if (!K->mgs[k]) {
     cudaGraph_t g = nullptr;
     MH_CHECK_CUDA(cudaStreamBeginCapture(K->gs, cudaStreamCaptureModeThreadLocal));
-    const int st_enq = enqueue_mgs(K->gs, K, n, k);
+    const int st_enq = enqueue_mgs(K->gs, K, n, k, false);
     const cudaError_t ce = cudaStreamEndCapture(K->gs, &g);
     MH_CHECK(st_enq);
     MH_CHECK_CUDA(ce);
     MH_CHECK_CUDA(cudaGraphInstantiate(&K->mgs[k], g, 0));
     cudaGraphDestroy(g);
   }
-  MH_CHECK_CUDA(cudaEventRecord(K->ev_in, st));
-  MH_CHECK_CUDA(cudaStreamWaitEvent(K->gs, K->ev_in, 0));
-  MH_CHECK_CUDA(cudaGraphLaunch(K->mgs[k], K->gs));
-  MH_CHECK_CUDA(cudaEventRecord(K->ev_out, K->gs));
-  MH_CHECK_CUDA(cudaStreamWaitEvent(st, K->ev_out, 0));
-  MH_CHECK_CUDA(cudaEventSynchronize(K->ev_out));
+  MH_CHECK_CUDA(cudaGraphLaunch(K->mgs[k], st));  // captured on gs, launched in order on st
   return MH_OK;
 }
 
@@ -358,10 +621,6 @@ int gmres_core(cudaStream_t st, Krylov* K, int64_t n, const OpFn& A, const OpFn&
     return MH_OK;
   }
   const int m = restart;
-  const char* gv = getenv("MEHDG_GMRES_GRAPHS");
-  const bool use_graphs = K->persistent &&
-                          !(g_comm_sys && (g_comm_sys->nranks > 1 || g_comm_sys->nccl)) &&
-                          !(gv && gv[0] == '0');
   std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), y(m);
   auto Hat = [&](int i, int k) -> double& { return H[(size_t)i * m + k]; };
   double* V = K->V.p;
@@ -396,14 +655,9 @@ int gmres_core(cudaStream_t st, Krylov* K, int64_t n, const OpFn& A, const OpFn&
     for (int k = 0; k < m; ++k) {
       double* Vk = V + (size_t)k * n;
       MH_CHECK(apply_MA(A, M, MA, Vk, K->w.p, K->tmp.p));
-      // MGS: H[i,k] = V[i].w ; w -= H[i,k] V[i]   (fused one step behind), as one
-      // CUDA graph per k on a single device (the multi-rank dots go through NCCL)
-      if (use_graphs) {
-        MH_CHECK(run_mgs(st, K, n, k));
-      } else {
-        MH_CHECK(enqueue_mgs(st, K, n, k));
-        MH_CHECK_CUDA(cudaStreamSynchronize(st));
-      }
+      // MGS: H[i,k] = V[i].w ; w -= H[i,k] V[i]   (fused one step behind)
+      MH_CHECK(enqueue_mgs(st, K, n, k));
+      MH_CHECK_CUDA(cudaStreamSynchronize(st));
       for (int i = 0; i <= k + 1; ++i) Hat(i, k) = K->h_host[i];
       if (!(Hat(k + 1, k) > 1e-300)) breakdown = true;
       for (int i = 0; i < k; ++i) {
@@ -466,6 +720,207 @@ int gmres_core(cudaStream_t st, Krylov* K, int64_t n, const OpFn& A, const OpFn&
   return MH_OK;
 }
 
+// The same solve for operators that run on the device (a system's apply /
+// preconditioner): the Arnoldi steps are enqueued ahead -- chunks of kAhead,
+// the host reading the control block of the previous chunk while the next one
+// runs -- and the Givens rotations run on the device (givens_kernel), so no
+// host round trip sits between two steps.  Steps enqueued after the cycle
+// stopped are no-ops (the element / face / dot kernels read the stop flag).
+// The restart-cycle logic, the triangular solve for y (host, double) and the
+// final true-residual recheck are gmres_core's.
+constexpr int kAhead = 2;
+
+int gmres_pipelined(mh_system* s, cudaStream_t st, Krylov* K, int64_t n, const OpFn& A,
+                    const OpFn& M, const OpFn& MA, double tol, int restart, int maxiter,
+                    const double* rhs, double* x, int* iterations, int* converged,
+                    double* hist_host, int hist_cap, int* hist_len) {
+  std::vector<double> history;
+  MH_CHECK_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, st));
+  const double* mb = rhs;
+  if (M.fn) {
+    MH_CHECK(M(rhs, K->tmp.p));
+    mb = K->tmp.p;
+  }
+  MH_CHECK(dot_dev(st, K, n, const_cast<double*>(mb), nullptr, nullptr, nullptr, 2, K->scal.p));
+  MH_CHECK(read_scalars(st, K, K->scal.p, 1));
+  const double bnorm = K->h_host[0];
+  int it = 0;
+  bool conv = false;
+  auto finish = [&](void) {
+    if (iterations) *iterations = it;
+    if (converged) *converged = conv ? 1 : 0;
+    if (hist_len) *hist_len = (int)history.size();
+    if (hist_host)
+      for (int i = 0; i < (int)history.size() && i < hist_cap; ++i) hist_host[i] = history[i];
+  };
+  if (bnorm == 0.0) {
+    history.push_back(0.0);
+    conv = true;
+    finish();
+    return MH_OK;
+  }
+  const int m = restart;
+  const bool multi = g_comm_sys && (g_comm_sys->nranks > 1 || g_comm_sys->nccl);
+  const bool use_graphs = !multi && proc_knobs().gmres_graphs;
+  std::vector<double> H((size_t)(m + 1) * m), g(m + 1), y(m), hist(m);
+  auto Hat = [&](int i, int k) -> double& { return H[(size_t)i * m + k]; };
+  double* V = K->V.p;
+  const dim3 vg(kVecGrid), vb(kVecThreads);
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  for (auto& e : ev) MH_CHECK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  struct Guard {  // clear the stop flag's users and the events on every exit
+    mh_system* s;
+    Krylov* K;
+    cudaEvent_t* ev;
+    ~Guard() {
+      s->skip = nullptr;
+      K->skip = nullptr;
+      for (int i = 0; i < 2; ++i) cudaEventDestroy(ev[i]);
+    }
+  } guard{s, K, ev};
+  // MEHDG_GMRES_TRACE: CUDA events around each step's apply / MGS / Givens,
+  // the summed times printed to stderr (design measurements only)
+  struct Trace {
+    bool on = getenv("MEHDG_GMRES_TRACE") != nullptr;
+    std::vector<std::pair<int, cudaEvent_t>> ev;
+    void mark(cudaStream_t st, int tag) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      cudaEventRecord(e, st);
+      ev.emplace_back(tag, e);
+    }
+    ~Trace() {
+      if (!on) return;
+      cudaDeviceSynchronize();
+      double t[4] = {0, 0, 0, 0};
+      for (size_t i = 1; i < ev.size(); ++i) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev[i - 1].second, ev[i].second);
+        t[ev[i - 1].second ? ev[i - 1].first : 0] += ms;
+      }
+      fprintf(stderr, "gmres trace: apply %.3f ms, mgs %.3f ms, givens %.3f ms, gaps %.3f ms (%zu marks)\n",
+              t[0], t[1], t[2], t[3], ev.size());
+      for (auto& pr : ev) cudaEventDestroy(pr.second);
+    }
+  } tr;
+  bool x_zero = true;
+  while (it < maxiter && !conv) {
+    // r = M(b - A x), beta (host: the cycle's start and stop tests); with x = 0
+    // (the first cycle) A x = 0 exactly and r = M b, already formed for bnorm
+    double* r;
+    if (x_zero) {
+      r = M.fn ? K->tmp.p : const_cast<double*>(rhs);
+    } else {
+      MH_CHECK(A(x, K->tmp.p));
+      sub_kernel<<<vg, vb, 0, st>>>(n, rhs, K->tmp.p, K->tmp2.p);
+      MH_CHECK_CUDA(cudaGetLastError());
+      r = K->tmp2.p;
+      if (M.fn) {
+        MH_CHECK(M(K->tmp2.p, K->w.p));
+        r = K->w.p;
+      }
+    }
+    MH_CHECK(dot_dev(st, K, n, r, nullptr, nullptr, nullptr, 2, K->scal.p));
+    MH_CHECK(read_scalars(st, K, K->scal.p, 1));
+    const double beta = K->h_host[0];
+    if (history.empty()) history.push_back(beta);
+    if (beta / bnorm <= tol) {
+      conv = true;
+      break;
+    }
+    // the cycle's device state: H = cs = sn = g = 0, g[0] = beta, control block
+    MH_CHECK_CUDA(cudaMemsetAsync(K->Hd.p, 0, sizeof(double) * (size_t)(m + 1) * m, st));
+    MH_CHECK_CUDA(cudaMemsetAsync(K->csd.p, 0, sizeof(double) * m, st));
+    MH_CHECK_CUDA(cudaMemsetAsync(K->snd.p, 0, sizeof(double) * m, st));
+    MH_CHECK_CUDA(cudaMemsetAsync(K->gd.p, 0, sizeof(double) * (m + 1), st));
+    K->h_host[0] = beta;
+    MH_CHECK_CUDA(cudaMemcpyAsync(K->gd.p, K->h_host, sizeof(double), cudaMemcpyHostToDevice, st));
+    int* ch = K->ctl_host;
+    for (int i = 0; i < kCtlInts; ++i) ch[i] = 0;
+    ch[kIt] = it;
+    MH_CHECK_CUDA(cudaMemcpyAsync(K->ctl.p, ch, sizeof(int) * kCtlInts, cudaMemcpyHostToDevice, st));
+    scale_kernel<<<vg, vb, 0, st>>>(n, r, beta, V);
+    MH_CHECK_CUDA(cudaGetLastError());
+    MH_CHECK_CUDA(cudaStreamSynchronize(st));  // pinned buffers reused below
+    K->skip = K->ctl.p + kStop;
+    s->skip = K->skip;
+    int k = 0, chunk = 0;
+    bool stopped = false;
+    while (k < m && !stopped) {
+      const int k1 = std::min(m, k + kAhead);
+      for (; k < k1; ++k) {
+        double* Vk = V + (size_t)k * n;
+        if (tr.on) tr.mark(st, 0);
+        MH_CHECK(apply_MA(A, M, MA, Vk, K->w.p, K->tmp.p));
+        if (tr.on) tr.mark(st, 1);
+        if (use_graphs) MH_CHECK(run_mgs(st, K, n, k));
+        else MH_CHECK(enqueue_mgs(st, K, n, k, false));
+        if (tr.on) tr.mark(st, 2);
+        givens_kernel<<<1, 32, 0, st>>>(K->hcol.p, K->Hd.p, K->csd.p, K->snd.p, K->gd.p,
+                                       K->histd.p, K->ctl.p, k, m, bnorm, tol, maxiter);
+        MH_CHECK_CUDA(cudaGetLastError());
+        if (tr.on) tr.mark(st, 3);
+      }
+      const int slot = chunk & 1;
+      MH_CHECK_CUDA(cudaMemcpyAsync(ch + 8 * slot, K->ctl.p, sizeof(int) * kCtlInts,
+                                    cudaMemcpyDeviceToHost, st));
+      MH_CHECK_CUDA(cudaEventRecord(ev[slot], st));
+      if (chunk > 0) {  // the previous chunk's control block, while this one runs
+        MH_CHECK_CUDA(cudaEventSynchronize(ev[slot ^ 1]));
+        stopped = ch[8 * (slot ^ 1) + kStop] != 0;
+      }
+      ++chunk;
+    }
+    MH_CHECK_CUDA(cudaStreamSynchronize(st));
+    s->skip = nullptr;
+    K->skip = nullptr;
+    // the cycle's outcome to the host
+    MH_CHECK_CUDA(cudaMemcpy(ch, K->ctl.p, sizeof(int) * kCtlInts, cudaMemcpyDeviceToHost));
+    const int k_used = ch[kKUsed], steps = ch[kSteps];
+    it = ch[kIt];
+    conv = ch[kConv] != 0;
+    const bool breakdown = ch[kBreak] != 0;
+    if (steps > 0) {
+      MH_CHECK_CUDA(cudaMemcpy(hist.data(), K->histd.p, sizeof(double) * steps, cudaMemcpyDeviceToHost));
+      history.insert(history.end(), hist.begin(), hist.begin() + steps);
+    }
+    if (k_used > 0) {
+      MH_CHECK_CUDA(cudaMemcpy(H.data(), K->Hd.p, sizeof(double) * (size_t)(m + 1) * m,
+                               cudaMemcpyDeviceToHost));
+      MH_CHECK_CUDA(cudaMemcpy(g.data(), K->gd.p, sizeof(double) * (m + 1), cudaMemcpyDeviceToHost));
+      // y = solve_triangular(H[:k,:k], g[:k]) (upper, column-oriented like dtrsv)
+      for (int j = 0; j < k_used; ++j) y[j] = g[j];
+      for (int j = k_used - 1; j >= 0; --j) {
+        y[j] = y[j] / Hat(j, j);
+        for (int i = 0; i < j; ++i) y[i] -= y[j] * Hat(i, j);
+      }
+      for (int j = 0; j < k_used; ++j) K->h_host[j] = y[j];
+      MH_CHECK_CUDA(cudaMemcpyAsync(K->ydev.p, K->h_host, sizeof(double) * k_used,
+                                    cudaMemcpyHostToDevice, st));
+      update_x_kernel<<<vg, vb, 0, st>>>(n, k_used, V, K->ydev.p, x);
+      MH_CHECK_CUDA(cudaGetLastError());
+      MH_CHECK_CUDA(cudaStreamSynchronize(st));  // h_host reused below
+      x_zero = false;
+    }
+    if (breakdown && !conv) break;  // invariant Krylov subspace
+  }
+  if (!conv) {  // one true-residual recheck (schur_solver.py:382-384)
+    MH_CHECK(A(x, K->tmp.p));
+    sub_kernel<<<vg, vb, 0, st>>>(n, rhs, K->tmp.p, K->tmp2.p);
+    MH_CHECK_CUDA(cudaGetLastError());
+    double* r = K->tmp2.p;
+    if (M.fn) {
+      MH_CHECK(M(K->tmp2.p, K->w.p));
+      r = K->w.p;
+    }
+    MH_CHECK(dot_dev(st, K, n, r, nullptr, nullptr, nullptr, 2, K->scal.p));
+    MH_CHECK(read_scalars(st, K, K->scal.p, 1));
+    conv = K->h_host[0] / bnorm <= tol;
+  }
+  finish();
+  return MH_OK;
+}
+
 // ---- system operators ------------------------------------------------------
 int sys_apply(void* ctx, const double* in, double* out) { return mh_apply((mh_system*)ctx, in, out); }
 int sys_apply_mb(void* ctx, const double* in, double* out) {
@@ -490,12 +945,13 @@ extern "C" int mh_dot(void* stream, int64_t n, const double* x, const double* y,
   }
   cudaStream_t st = (cudaStream_t)stream;
   Krylov K;
-  MH_CHECK(K.part.alloc(kDotBlocks));
+  MH_CHECK(K.part.alloc(kDotPartsMax));
   MH_CHECK(K.ticket.alloc(1));
   MH_CHECK(K.scal.alloc(1));
   MH_CHECK_CUDA(cudaMemsetAsync(K.ticket.p, 0, sizeof(unsigned), st));
-  dot_kernel<<<kDotBlocks, kDotThreads, 0, st>>>(n, const_cast<double*>(x), nullptr, nullptr, y, 0,
-                                                  true, K.part.p, K.ticket.p, K.scal.p);
+  dot_kernel<<<dot_parts(n) / kDotWarps, kDotWarps * 32, 0, st>>>(
+      n, const_cast<double*>(x), nullptr, nullptr, y, 0, true, K.part.p, K.ticket.p, K.scal.p,
+      nullptr);
   MH_CHECK_CUDA(cudaGetLastError());
   MH_CHECK_CUDA(cudaMemcpyAsync(out, K.scal.p, sizeof(double), cudaMemcpyDeviceToHost, st));
   MH_CHECK_CUDA(cudaStreamSynchronize(st));
@@ -549,8 +1005,11 @@ extern "C" int mh_gmres(mh_system* s, double tol, int restart, int maxiter, int 
     }
   }
   CommScope scope(s);
-  return gmres_core(s->stream, s->kry, n, A, M, MA, tol, restart, maxiter, rhs, x, iterations,
-                    converged, hist_host, hist_cap, hist_len);
+  if (restart > kMaxRestartSmem)  // beyond the device Givens' staging: the host loop
+    return gmres_core(s->stream, s->kry, n, A, M, MA, tol, restart, maxiter, rhs, x, iterations,
+                      converged, hist_host, hist_cap, hist_len);
+  return gmres_pipelined(s, s->stream, s->kry, n, A, M, MA, tol, restart, maxiter, rhs, x,
+                         iterations, converged, hist_host, hist_cap, hist_len);
 }
 
 extern "C" int mh_gmres_op(int device, void* stream, int64_t n, mh_op_fn apply, void* apply_ctx,

@@ -440,11 +440,8 @@ int launch_nt(mh_system* s, const LuArgs& g, cudaEvent_t start) {
   per_sm = std::max(per_sm, 1);
   // resident CTAs per SM: 3 (12 warps) measured best at c2 / c3 -- more warps
   // hide more latency but their scratch slots crowd L2 (MEHDG_LU_CTAS overrides)
-  const char* cv = getenv("MEHDG_LU_CTAS");
-  per_sm = std::max(1, std::min(per_sm, cv ? atoi(cv) : 3));
-  const char* sp = getenv("MEHDG_LU_SCR");
-  const char* ap = getenv("MEHDG_LU_APOL");
-  const int scr_pol = sp ? atoi(sp) : 0, a_pol = ap ? atoi(ap) : 1;
+  per_sm = std::max(1, std::min(per_sm, s->knobs.lu_ctas));
+  const int scr_pol = s->knobs.lu_scr_pol, a_pol = s->knobs.lu_a_pol;
   const int64_t need = (g.nblocks + kTileWarps - 1) / kTileWarps;
   const int64_t grid = std::min<int64_t>(need, (int64_t)per_sm * s->num_sms);
   MH_CHECK(s->lu_scr.alloc((size_t)grid * kTileWarps * S::kSlotDoubles));

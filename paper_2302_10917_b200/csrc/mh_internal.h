@@ -36,8 +36,6 @@ constexpr int kWarp = 32;
 constexpr int kMaxSlots = 6;
 constexpr unsigned kFull = 0xffffffffu;
 // fixed reduction partition: results never depend on the device or SM count
-constexpr int kDotBlocks = 512;
-constexpr int kDotThreads = 256;
 // chunk (doubles) of the element kernel's bulk-copy stream; the per-macro
 // strides of the streamed arrays (op.B^T, L, U, op.C) are multiples of it
 constexpr int kStreamChunk = 512;
@@ -69,9 +67,27 @@ struct DBuf {
 
 struct Krylov;  // GMRES workspace (krylov.cu)
 
+// Tuning knobs: read from the environment once, when a
+// system is created, never on a launch path.  Defaults are the measured best.
+struct Knobs {
+  int lu = 0;             // MEHDG_LU: 0 default, 1 tile, 2 cta
+  int lu_ctas = 3;        // MEHDG_LU_CTAS: resident CTAs per SM of the tile LU
+  int lu_scr_pol = 0;     // MEHDG_LU_SCR: L2 policy of the tile LU's scratch
+  int lu_a_pol = 1;       // MEHDG_LU_APOL: L2 policy of the A stream (1 evict_first)
+  int elem_ctas = 0;      // MEHDG_ELEM_CTAS: cap on element-kernel CTAs per SM (0: none)
+  int elem_ch = 512;      // MEHDG_ELEM_CH: element stream chunk (doubles)
+  int mgs_small = 1;      // MEHDG_MGS_SMALL: the MGS block of a step as one kernel
+  int mgs_ctas = 4;       // MEHDG_MGS_CTAS: its CTAs per SM (at most)
+  int mgs_reg = 1;        // MEHDG_MGS_REG: w held in registers when it fits
+  int gmres_graphs = 1;   // MEHDG_GMRES_GRAPHS: MGS block as a CUDA graph
+  int64_t split_at = -1;  // MEHDG_SPLIT_AT: interior/halo macro split (-1: computed)
+  void read();
+};
+
 }  // namespace mh
 
 struct mh_system {
+  mh::Knobs knobs;
   int device = 0;
   int nfe = 3;        // faces (slots) per macro = d+1
   int64_t N = 0;      // macros on this device
@@ -98,7 +114,6 @@ struct mh_system {
 
   // blocks
   mh::DBuf<double> A;      // staged A, N*Q*Q row-major (input of the LU)
-  mh::DBuf<double> LU;     // N*Q*Q column-major workspace (only when Q*Q*8 > smem)
   mh::DBuf<double> lu_scr; // per-warp-slot scratch of the tile LU (inverse diagonal blocks)
   mh::DBuf<double> Lp;     // N*ldL packed strict lower L, columns 0..Q-2 (streamed)
   mh::DBuf<double> Up;     // N*ldL packed strict upper U, columns Q-1..1 (streamed)
@@ -124,6 +139,9 @@ struct mh_system {
   mh::DBuf<double> hin, hout;  // staging for the *_host entry points
 
   mh::Krylov* kry = nullptr;
+  // set while a pipelined GMRES cycle runs: the element / face kernels of a
+  // step enqueued after the cycle stopped return at once
+  const int* skip = nullptr;
 
   // optional per-kernel event timing (mh_profile)
   bool profiling = false;
@@ -146,6 +164,10 @@ struct mh_system {
 };
 
 namespace mh {
+// capi.cu: resident CTAs per SM of `kern` at (threads, smem); sets the
+// function's max-dynamic-smem attribute (raise-only, process-wide cache);
+// -1 (error set) on failure
+int launch_occupancy(int device, const void* kern, int threads, size_t smem);
 // lu.cu
 int launch_lu(mh_system* s, float* ms);
 // element.cu

@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import csv
 import io
+import os
 from typing import Sequence
 
 import numpy as np
@@ -37,33 +38,37 @@ def export_text(mesh) -> str:
     return "\n".join(lines) + "\n"
 
 
-def _fmt(v) -> str:
-    if v is None:
+def _cell(value) -> str:
+    """One CSV cell of the report convention: None -> empty, a float (Python or
+    numpy) with 17 significant digits so that it reads back to the same double,
+    anything else (bools, ints, strings) through str()."""
+    if value is None:
         return ""
-    if isinstance(v, bool):
-        return str(v)
-    if isinstance(v, (float, np.floating)):
-        return "%.17g" % float(v)
-    return str(v)
+    if isinstance(value, (float, np.floating)):
+        return format(float(value), ".17g")
+    return str(value)
+
+
+def _table(rows, columns):
+    """Header, then one line per record in column order (missing keys empty)."""
+    yield list(columns)
+    for record in rows:
+        yield [_cell(record.get(name)) for name in columns]
 
 
 def write_csv(rows: list, columns: Sequence[str], out) -> None:
-    own = isinstance(out, (str, bytes))
-    fh = open(out, "w", newline="") if own else out
-    try:
-        writer = csv.writer(fh)
-        writer.writerow(columns)
-        for row in rows:
-            writer.writerow([_fmt(row.get(c)) for c in columns])
-    finally:
-        if own:
-            fh.close()
+    """Report rows to a CSV file (path) or an open text stream."""
+    if isinstance(out, (str, bytes, os.PathLike)):
+        with open(out, "w", newline="") as fh:
+            csv.writer(fh).writerows(_table(rows, columns))
+    else:
+        csv.writer(out).writerows(_table(rows, columns))
 
 
 def rows_to_csv(rows: list, columns: Sequence[str]) -> str:
-    buf = io.StringIO()
-    write_csv(rows, columns, buf)
-    return buf.getvalue()
+    sink = io.StringIO()
+    csv.writer(sink).writerows(_table(rows, columns))
+    return sink.getvalue()
 
 
 def _parse(raw: str):

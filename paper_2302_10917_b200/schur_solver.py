@@ -237,6 +237,106 @@ class CondensedSystem:
 
 
 # ---------------------------------------------------------------------------
+# the factors the reference stores in its operator objects
+
+class _DeviceLU:
+    """``op.lu`` of a condensed macro: ``("dense", (lu, piv))`` in scipy's layout,
+    fetched from the device on first access (the reference stores it at
+    condense, schur_solver.py:111)."""
+
+    __slots__ = ("_sys", "_e", "_val")
+
+    def __init__(self, sys, e):
+        self._sys, self._e, self._val = sys, e, None
+
+    def _get(self):
+        if self._val is None:
+            lu, piv = local_factors(self._sys, self._e, 1)
+            self._val = ("dense", (lu[0], piv[0]))
+        return self._val
+
+    def __getitem__(self, i):
+        return self._get()[i]
+
+    def __len__(self):
+        return 2
+
+    def __iter__(self):
+        return iter(self._get())
+
+    def __repr__(self):
+        return f"_DeviceLU(macro={self._e})"
+
+
+class _DeviceFaceFactor:
+    """``op.factor`` of a condensed face: ``("inv", 1.0, D^-1)`` -- the explicit
+    inverse the device preconditioner applies (sign folded in) -- fetched on
+    first access.  Replacing ``op.factor`` after condense (as the reference's
+    tests do, test_schur_solver.py:138-147) is honoured by
+    ``apply_preconditioner``: the replaced faces' inverses are recomputed from
+    the new factor with the reference's solve rule and uploaded."""
+
+    __slots__ = ("_sys", "_u", "_val")
+
+    def __init__(self, sys, u):
+        self._sys, self._u, self._val = sys, u, None
+
+    def _get(self):
+        if self._val is None:
+            t = self._sys.t
+            inv = np.empty((1, t, t))
+            check(lib.mh_get_face_inverse(self._sys.handle, 1, ptr(np.array([self._u], np.int32)),
+                                          ptr(inv)), "mh_get_face_inverse")
+            self._val = ("inv", 1.0, inv[0])
+        return self._val
+
+    def __getitem__(self, i):
+        return self._get()[i]
+
+    def __len__(self):
+        return 3
+
+    def __iter__(self):
+        return iter(self._get())
+
+    def __repr__(self):
+        return f"_DeviceFaceFactor(face={self._u})"
+
+
+def _face_inverse_from_factor(factor, t):
+    """D^-1 (sign folded in) from a reference face factor (schur_solver.py:150-154)."""
+    import scipy.linalg as sla
+
+    kind, sign, fac = factor
+    eye = np.eye(t)
+    if kind == "chol":
+        return sign * sla.cho_solve(fac, eye)
+    if kind == "inv":
+        return sign * np.asarray(fac)
+    return sla.lu_solve(fac, eye)
+
+
+def _sync_face_factors(sys) -> None:
+    """Upload the inverses of faces whose ``op.factor`` was replaced since condense."""
+    if sys.face_ops is None:
+        return
+    idx, inv = [], []
+    for u, fid in enumerate(sys.face_ids):
+        fop = sys.face_ops[int(fid)]
+        fac = getattr(fop, "factor", None)
+        if isinstance(fac, _DeviceFaceFactor) and fac._sys is sys:
+            continue
+        idx.append(u)
+        inv.append(_face_inverse_from_factor(fac, sys.t))
+        fop.factor = _DeviceFaceFactor(sys, u)
+        fop.factor._val = ("inv", 1.0, inv[-1])
+    if idx:
+        arr = np.ascontiguousarray(np.stack(inv))
+        check(lib.mh_set_face_inverse(sys.handle, len(idx), ptr(np.asarray(idx, np.int32)),
+                                      ptr(arr)), "mh_set_face_inverse")
+
+
+# ---------------------------------------------------------------------------
 # condense
 
 def _stack_ops(local_ops: list, face_ops: dict, tables: dict):
@@ -370,13 +470,17 @@ def condense(mesh, local_ops: list, face_ops: dict, config: SolverConfig,
     m = mesh.macro_elements[0].m if len(mesh.macro_elements) else 1
     sys = condense_arrays(mesh, A, B, Cm, Ru, D, Rh, config, p=_infer_p(nloc, m),
                           tables=tables, local_ops=local_ops, face_ops=face_ops, pool=pool)
+    # the reference's in-place factor fields (schur_solver.py:111, 137-147):
+    # device-backed, fetched on access; host_factors=True fetches them now
     if host_factors:
         lu, piv = local_factors(sys)
         for e, op in enumerate(local_ops):
             op.lu = ("dense", (lu[e], piv[e]))
-        for u, fid in enumerate(sys.face_ids):
-            fop = face_ops[int(fid)]
-            fop.factor = ("inv", 1.0, np.linalg.inv(fop.D))
+    else:
+        for e, op in enumerate(local_ops):
+            op.lu = _DeviceLU(sys, e)
+    for u, fid in enumerate(sys.face_ids):
+        face_ops[int(fid)].factor = _DeviceFaceFactor(sys, u)
     return sys
 
 
@@ -472,7 +576,9 @@ def apply_schur_many(sys: CondensedSystem, U, out=None, repeat: Optional[int] = 
 
 
 def apply_preconditioner(sys: CondensedSystem, w):
-    """Per-face D^-1 (schur_solver.py:296-305)."""
+    """Per-face D^-1 (schur_solver.py:296-305), with the face factors in
+    ``sys.face_ops`` -- including ones replaced after condense."""
+    _sync_face_factors(sys)
     return _run(sys, lib.mh_precond, "mh_precond", w)
 
 
@@ -522,6 +628,8 @@ def gmres(apply_op: Callable, rhs, config: SolverConfig, precond: Optional[Calla
     torch = _torch()
     sysA, mode = _bound_system(apply_op, "A")
     sysM, _ = _bound_system(precond, "M") if precond is not None else (None, None)
+    if sysM is not None:
+        _sync_face_factors(sysM)
     host = not _is_torch(rhs)
     n = int(rhs.numel() if not host else np.asarray(rhs).size)
     cap = config.maxiter + 2
@@ -735,10 +843,22 @@ def solve_condensed(sys: CondensedSystem, config: SolverConfig, t_init: float = 
     if config.mode == "mb":
         form_element_schur(sys)
     op = SchurOperator(sys, config.mode)
-    sys.timings["local"] = 0.0
+    # t_local: the element kernels' time inside the solve (CUDA events around
+    # each launch, mh_profile) -- the reference sums its local tasks' time the
+    # same way (schur_solver.py:518-535); t_global is the rest of GMRES
+    h = sys.handle
+    check(lib.mh_profile_read(h, None, None, None, None), "profile")
+    check(lib.mh_profile(h, 1), "profile")
     t0 = time.perf_counter()
-    uhat, info = gmres(op, sys.f_device, config, precond=precond)
-    t_gmres = time.perf_counter() - t0
+    try:
+        uhat, info = gmres(op, sys.f_device, config, precond=precond)
+    finally:
+        t_gmres = time.perf_counter() - t0
+        ems = C.c_double()
+        check(lib.mh_profile_read(h, C.byref(ems), None, None, None), "profile")
+        check(lib.mh_profile(h, 0), "profile")
+    t_local = ems.value / 1e3
+    sys.timings["local"] = t_local
     t0 = time.perf_counter()
     U = reconstruct_interior(sys, uhat)
     local = list(U.cpu().numpy())
@@ -749,7 +869,8 @@ def solve_condensed(sys: CondensedSystem, config: SolverConfig, t_init: float = 
         n=getattr(mesh, "n", 0), dof_local=sys.dof_local, dof_global=sys.zhat,
         iterations=info["iterations"], converged=info["converged"], tol=config.tol,
         mode=config.mode, precond=config.preconditioner, t_init_s=t_init,
-        t_local_s=0.0, t_global_s=t_gmres, t_reconstruct_s=t_rec, lbf=sys.pool.lbf,
+        t_local_s=t_local, t_global_s=max(t_gmres - t_local, 0.0), t_reconstruct_s=t_rec,
+        lbf=sys.pool.lbf,
         worker_busy=list(sys.pool.busy), residual_history=info["residual_history"])
     return Solution(local=local, uhat=uhat.cpu().numpy(), report=report), sys
 

@@ -22,8 +22,8 @@ from __future__ import annotations
 import numpy as np
 
 from .mesh import build_structured_macro_mesh, condense_tables, mesh_tables
-from .synthetic_gen import (CHUNK, CONFIGS, block_sizes, gen_faces, gen_macros,  # noqa: F401
-                            gen_uhat)
+from .synthetic_gen import (CHUNK, CONFIGS, block_sizes, gen_faces, gen_faces_at,  # noqa: F401
+                            gen_macros, gen_uhat)
 
 
 def make_problem(d: int, n: int, m: int, p: int, seed: int = 0, with_blocks: bool = True,

@@ -97,3 +97,23 @@ def gen_faces(F: int, t: int, seed: int = 0, first: int = 0, count: int = None):
 
 def gen_uhat(zhat: int, seed: int = 0) -> np.ndarray:
     return np.random.default_rng([seed, 2]).standard_normal(zhat)
+
+
+def gen_faces_at(F: int, t: int, seed: int, idx) -> np.ndarray:
+    """The face blocks of the unknown faces `idx` only (a rank's owned faces):
+    each CHUNK of faces that holds one of them is drawn once, the same stream
+    as gen_faces(F, t, seed)[idx]."""
+    idx = np.asarray(idx, dtype=np.int64)
+    out = np.empty((idx.size, t, t))
+    which = idx // CHUNK
+    chunks = np.unique(which)
+
+    def work(c):
+        lo = int(c) * CHUNK
+        Dc = gen_faces(F, t, seed, lo, min(CHUNK, F - lo))
+        sel = which == c
+        out[sel] = Dc[idx[sel] - lo]
+
+    with cf.ThreadPoolExecutor(_threads(chunks.size)) as ex:
+        list(ex.map(work, chunks))
+    return out

@@ -67,9 +67,8 @@ def test_single_rank_nccl_communicator(gpu, split, monkeypatch):
     halo exchange; [0, split) after it)."""
     if split is not None:
         monkeypatch.setenv("MEHDG_SPLIT_AT", str(split))
-    # the multi-rank GMRES uses the grid-wide dot kernels; the plain system would
-    # take the one-CTA MGS for a vector this short (same math, other summation tree)
-    monkeypatch.setenv("MEHDG_MGS_SMALL", "0")
+    # the multi-rank GMRES uses the grid-wide dot kernels, the plain system the
+    # one-CTA MGS for a vector this short: the same partials in the same order
     prob = S.make_problem(2, 8, 2, 3, seed=4)
     pl = rank_plan(prob["elem_face"], prob["face_elem"], prob["face_slot"],
                    np.array([0, prob["N"]]), 0)

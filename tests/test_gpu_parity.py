@@ -422,5 +422,8 @@ def test_host_factors_and_solve_driver(gpu):
     sol, sys2 = P.solve(mesh, None, None, P.SolverConfig(tol=1e-12), p, assemble=assemble)
     rec = sol.report.to_record()
     assert rec["converged"] and abs(rec["iterations"] - int(g["iterations"])) <= 1
+    # the local/global split of the solve time (schur_solver.py:518-535): the
+    # element kernels' event time, and the rest of GMRES
+    assert 0.0 < rec["t_local_s"] and rec["t_global_s"] >= 0.0
     assert rel(sol.uhat, g["x"]) <= SOLVE_TOL
     assert rel(np.stack(sol.local), g["U"]) <= SOLVE_TOL

@@ -99,3 +99,14 @@ def test_slab_oracle_equals_whole_mesh_on_complete_faces():
             assert np.allclose(o.rhs().reshape(-1, t)[complete],
                                ff.reshape(-1, t)[fidx[complete]], rtol=0, atol=1e-12)
             assert not np.allclose(ws[~complete], wf.reshape(-1, t)[fidx[~complete]])
+
+
+def test_owned_face_generation_matches_whole_mesh_draw():
+    """A rank draws only its owned faces' blocks (synthetic_gen.gen_faces_at) --
+    the same numbers as the whole-mesh draw, whatever chunks they fall in."""
+    from paper_2302_10917_b200 import synthetic_gen as G
+
+    rng = np.random.default_rng(2)
+    F = 3 * G.CHUNK + 17
+    idx = np.sort(rng.choice(F, 300, replace=False))
+    assert np.array_equal(G.gen_faces_at(F, 4, 5, idx), G.gen_faces(F, 4, 5)[idx])
