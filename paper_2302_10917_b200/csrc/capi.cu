@@ -145,6 +145,7 @@ void Knobs::read() {
   if (const char* v = env("MEHDG_MGS_SMALL")) mgs_small = atoi(v);
   if (const char* v = env("MEHDG_MGS_CTAS")) mgs_ctas = std::max(1, atoi(v));
   if (const char* v = env("MEHDG_MGS_REG")) mgs_reg = atoi(v);
+  if (const char* v = env("MEHDG_FACE_BULK")) face_bulk = atoi(v);
   if (const char* v = env("MEHDG_GMRES_GRAPHS")) gmres_graphs = atoi(v);
   if (const char* v = env("MEHDG_SPLIT_AT")) split_at = atoll(v);
 }
@@ -288,10 +289,11 @@ static int alloc_blocks(mh_system* s) {
   MH_CHECK(s->lstat.alloc(N));
   MH_CHECK(s->Bt.alloc(N * (size_t)s->ldB));
   MH_CHECK(s->Ru.alloc(N * Q));
-  MH_CHECK(s->D.alloc(F * t * t));
+  s->ldF = ((int64_t)t * t + 1) & ~int64_t(1);
+  MH_CHECK(s->D.alloc(F * s->ldF));
   MH_CHECK(s->Draw.alloc(F * t * t));
   MH_CHECK(s->Rhat.alloc(F * t));
-  MH_CHECK(s->Dinv.alloc(F * t * t));
+  MH_CHECK(s->Dinv.alloc(F * s->ldF));
   MH_CHECK(s->Fkind.alloc(F));
   MH_CHECK(s->V.alloc((N * s->nfe + (size_t)s->n_vslot_extra) * t));
   MH_CHECK(s->tmp.alloc((F + (size_t)s->F_halo) * t + 1));
@@ -552,11 +554,11 @@ static int face_inverse_io(mh_system* s, int64_t n, const int32_t* idx, double* 
     if (set) {
       for (int i = 0; i < t; ++i)
         for (int j = 0; j < t; ++j) cm[(size_t)j * t + i] = hb[(size_t)i * t + j];
-      MH_CHECK_CUDA(cudaMemcpyAsync(s->Dinv.p + f * TT, cm.data(), sizeof(double) * TT,
+      MH_CHECK_CUDA(cudaMemcpyAsync(s->Dinv.p + f * s->ldF, cm.data(), sizeof(double) * TT,
                                     cudaMemcpyHostToDevice, s->stream));
       MH_CHECK_CUDA(cudaStreamSynchronize(s->stream));
     } else {
-      MH_CHECK_CUDA(cudaMemcpyAsync(cm.data(), s->Dinv.p + f * TT, sizeof(double) * TT,
+      MH_CHECK_CUDA(cudaMemcpyAsync(cm.data(), s->Dinv.p + f * s->ldF, sizeof(double) * TT,
                                     cudaMemcpyDeviceToHost, s->stream));
       MH_CHECK_CUDA(cudaStreamSynchronize(s->stream));
       for (int i = 0; i < t; ++i)

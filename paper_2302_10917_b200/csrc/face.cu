@@ -18,9 +18,11 @@
 // coalesced loads instead of a chain of 2t dependent substitution steps.
 // Face data layout: D and D^-1 column-major (t x t).
 
+#include <algorithm>
 #include <cfloat>
 
 #include "mh_internal.h"
+#include "stream.cuh"
 
 namespace mh {
 namespace {
@@ -36,6 +38,7 @@ struct FaceArgs {
   double* out;
   const double* Dinv;
   int64_t F;
+  int64_t ldF;  // per-face stride of D / D^-1 (t^2 rounded up to 16 bytes)
   int t;
   const int* skip;  // a stopped speculative GMRES step: return at once
 };
@@ -71,7 +74,6 @@ __global__ void __launch_bounds__(kFaceWarps * 32) face_reduce_kernel(FaceArgs a
   const int64_t f = (int64_t)blockIdx.x * kFaceWarps + w;
   if (f >= a.F) return;
   const int t = a.t;
-  const size_t TT = (size_t)t * t;
   double* sw = s_buf + w * t;
   double z[RT];
 #pragma unroll
@@ -93,7 +95,7 @@ __global__ void __launch_bounds__(kFaceWarps * 32) face_reduce_kernel(FaceArgs a
         if (sr >= 0) q[r] += __ldg(a.V + (int64_t)sr * t + i);
       }
     }
-    warp_gemv<RT>(q, a.Dinv + f * TT, t, sw, lane);
+    warp_gemv<RT>(q, a.Dinv + f * a.ldF, t, sw, lane);
 #pragma unroll
     for (int r = 0; r < RT; ++r) {
       const int i = lane + 32 * r;
@@ -101,7 +103,7 @@ __global__ void __launch_bounds__(kFaceWarps * 32) face_reduce_kernel(FaceArgs a
     }
     return;
   }
-  if (!RHS) warp_gemv<RT>(z, a.D + f * TT, t, sw, lane);  // D_f uhat_f
+  if (!RHS) warp_gemv<RT>(z, a.D + f * a.ldF, t, sw, lane);  // D_f uhat_f
 #pragma unroll
   for (int r = 0; r < RT; ++r) {
     const int i = lane + 32 * r;
@@ -110,11 +112,96 @@ __global__ void __launch_bounds__(kFaceWarps * 32) face_reduce_kernel(FaceArgs a
       if (sr >= 0) z[r] -= __ldg(a.V + (int64_t)sr * t + i);  // then right
     }
   }
-  if (PRE) warp_gemv<RT>(z, a.Dinv + f * TT, t, sw, lane);
+  if (PRE) warp_gemv<RT>(z, a.Dinv + f * a.ldF, t, sw, lane);
 #pragma unroll
   for (int r = 0; r < RT; ++r) {
     const int i = lane + 32 * r;
     if (i < t) a.out[f * t + i] = z[r];
+  }
+}
+
+// Faces with t > 32 (c4 t = 55, c5 t = 45), the apply and the fused M(A u):
+// each warp owns one face at a time and pulls its t x t block (16-24 KB,
+// contiguous, 16-byte aligned with the padded face stride) into shared memory
+// with one cp.async.bulk (TMA) while it loads the face's vectors; the GEMV then
+// reads the block from shared memory in the same order (columns ascending) as
+// warp_gemv, so the results are bitwise those of face_reduce_kernel.  A CTA
+// holds as many warps (blocks in flight) as ~200 KB of shared memory allows.
+template <int RT, bool PRE>
+__global__ void __launch_bounds__(8 * 32) face_bulk_kernel(FaceArgs a) {
+  if (a.skip && *a.skip) return;
+  extern __shared__ __align__(128) double s_bulk[];
+  __shared__ uint64_t mbar[8];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int t = a.t;
+  const int64_t ldF = a.ldF;
+  double* buf = s_bulk + (size_t)w * (ldF + 128);
+  double* sw = buf + ldF;
+  const uint32_t bytes = (uint32_t)(ldF * sizeof(double));
+  const double* Mbase = PRE ? a.Dinv : a.D;
+  if (lane == 0) {
+    mbar_init(&mbar[w], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  const uint64_t pol = l2_policy_evict_first();
+  uint32_t phase = 0;
+  for (int64_t f = (int64_t)blockIdx.x * nw + w; f < a.F; f += (int64_t)gridDim.x * nw) {
+    if (lane == 0) {
+      fence_proxy_async_smem();  // the previous face's reads before the copy's writes
+      mbar_expect_tx(&mbar[w], bytes);
+      bulk_g2s(buf, Mbase + f * ldF, bytes, &mbar[w], pol);
+    }
+    double z[RT], q[RT];
+    const int sl = __ldg(a.vslot + 2 * f), sr = __ldg(a.vslot + 2 * f + 1);
+#pragma unroll
+    for (int r = 0; r < RT; ++r) {
+      const int i = lane + 32 * r;
+      z[r] = i < t ? __ldg(a.uhat + f * t + i) : 0.0;
+      q[r] = 0.0;
+      if (PRE && i < t) {  // q = v_L + v_R (left first)
+        if (sl >= 0) q[r] = __ldg(a.V + (int64_t)sl * t + i);
+        if (sr >= 0) q[r] += __ldg(a.V + (int64_t)sr * t + i);
+      }
+    }
+    // the GEMV input: D^-1 applies to q (fused preconditioner), D to uhat_f
+#pragma unroll
+    for (int r = 0; r < RT; ++r) {
+      const int i = lane + 32 * r;
+      if (i < t) sw[i] = PRE ? q[r] : z[r];
+    }
+    __syncwarp();
+    while (!mbar_try_wait(&mbar[w], phase)) {
+    }
+    phase ^= 1;
+    double y[RT];
+#pragma unroll
+    for (int r = 0; r < RT; ++r) y[r] = 0.0;
+#pragma unroll 8
+    for (int s2 = 0; s2 < t; ++s2) {  // sum over columns ascending, as warp_gemv
+      const double ws = sw[s2];
+#pragma unroll
+      for (int r = 0; r < RT; ++r) {
+        const int i = lane + 32 * r;
+        if (i < t) y[r] = fma(buf[(size_t)s2 * t + i], ws, y[r]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < RT; ++r) {
+      const int i = lane + 32 * r;
+      if (i < t) {
+        double o;
+        if (PRE) {
+          o = z[r] - y[r];  // u_f - D_f^-1 (v_L + v_R)
+        } else {
+          o = y[r];
+          if (sl >= 0) o -= __ldg(a.V + (int64_t)sl * t + i);  // left first
+          if (sr >= 0) o -= __ldg(a.V + (int64_t)sr * t + i);  // then right
+        }
+        a.out[f * t + i] = o;
+      }
+    }
+    __syncwarp();
   }
 }
 
@@ -130,7 +217,6 @@ __global__ void __launch_bounds__(kFaceWarps * 32) face_small_kernel(FaceArgs a)
   const int64_t f = (int64_t)blockIdx.x * FPB + grp;
   const bool valid_face = f < a.F;
   const int t = a.t;
-  const size_t TT = (size_t)t * t;
   const bool row = valid_face && g < t;
   double* su = s_u + grp * G;
   double z = row ? __ldg((RHS ? a.Rhat : a.uhat) + f * t + g) : 0.0;
@@ -144,7 +230,7 @@ __global__ void __launch_bounds__(kFaceWarps * 32) face_small_kernel(FaceArgs a)
     }
     su[g] = q;
     __syncwarp(mask);
-    const double* Mi = a.Dinv + (valid_face ? f : 0) * TT;
+    const double* Mi = a.Dinv + (valid_face ? f : 0) * a.ldF;
     double acc = 0.0;
 #pragma unroll
     for (int s = 0; s < G; ++s)
@@ -155,7 +241,7 @@ __global__ void __launch_bounds__(kFaceWarps * 32) face_small_kernel(FaceArgs a)
   if (!RHS) {
     su[g] = z;
     __syncwarp(mask);
-    const double* Df = a.D + (valid_face ? f : 0) * TT;
+    const double* Df = a.D + (valid_face ? f : 0) * a.ldF;
     double acc = 0.0;
 #pragma unroll
     for (int s = 0; s < G; ++s)
@@ -171,7 +257,7 @@ __global__ void __launch_bounds__(kFaceWarps * 32) face_small_kernel(FaceArgs a)
   if (PRE) {
     su[g] = z;
     __syncwarp(mask);
-    const double* Mi = a.Dinv + (valid_face ? f : 0) * TT;
+    const double* Mi = a.Dinv + (valid_face ? f : 0) * a.ldF;
     double acc = 0.0;
 #pragma unroll
     for (int s = 0; s < G; ++s)
@@ -195,7 +281,7 @@ __global__ void __launch_bounds__(kFaceWarps * 32) precond_kernel(FaceArgs a) {
     const int i = lane + 32 * r;
     z[r] = i < t ? __ldg(a.uhat + f * t + i) : 0.0;
   }
-  warp_gemv<RT>(z, a.Dinv + f * (size_t)t * t, t, s_buf + w * t, lane);
+  warp_gemv<RT>(z, a.Dinv + f * a.ldF, t, s_buf + w * t, lane);
 #pragma unroll
   for (int r = 0; r < RT; ++r) {
     const int i = lane + 32 * r;
@@ -315,7 +401,7 @@ __device__ void warp_inverse(const double* S, const int* pm, int t, bool chol, d
 
 __global__ void face_factor_kernel(const double* __restrict__ Drm, double* __restrict__ Dcm,
                                    double* __restrict__ Dinv, int8_t* __restrict__ Fkind,
-                                   int64_t F, int t, int wpb) {
+                                   int64_t F, int t, int wpb, int64_t ldF) {
   extern __shared__ double s_fac[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t f = (int64_t)blockIdx.x * wpb + w;
@@ -329,7 +415,7 @@ __global__ void face_factor_kernel(const double* __restrict__ Drm, double* __res
   for (size_t idx = lane; idx < TT; idx += 32) {  // row-major in -> column-major copy
     const int i = (int)(idx / t), j = (int)(idx - (size_t)i * t);
     const double v = __ldg(Df + idx);
-    Dcm[f * TT + (size_t)j * t + i] = v;
+    Dcm[f * ldF + (size_t)j * t + i] = v;
     dmax = fmax(dmax, fabs(v));
   }
   for (int o = 16; o; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(kFull, dmax, o));
@@ -361,7 +447,7 @@ __global__ void face_factor_kernel(const double* __restrict__ Drm, double* __res
   }
   __syncwarp();
   if (kind != MH_FACE_SINGULAR)
-    warp_inverse(S, pm, t, kind != MH_FACE_LU, sign, scratch, Dinv + f * TT, lane);
+    warp_inverse(S, pm, t, kind != MH_FACE_LU, sign, scratch, Dinv + f * ldF, lane);
   if (lane == 0) Fkind[f] = (int8_t)kind;
 }
 
@@ -393,6 +479,7 @@ FaceArgs make_args(mh_system* s, const double* in, double* out) {
   a.uhat = in;
   a.out = out;
   a.Dinv = s->Dinv.p;
+  a.ldF = s->ldF;
   a.skip = s->skip;
   a.F = s->F;
   a.t = s->t;
@@ -435,7 +522,7 @@ int launch_face_factor(mh_system* s, const double* Drm) {
   }
   const unsigned grid = (unsigned)((s->F + wpb - 1) / wpb);
   face_factor_kernel<<<grid, wpb * 32, smem, s->stream>>>(Drm, s->D.p, s->Dinv.p, s->Fkind.p,
-                                                          s->F, t, wpb);
+                                                          s->F, t, wpb, s->ldF);
   MH_CHECK_CUDA(cudaGetLastError());
   return MH_OK;
 }
@@ -460,6 +547,25 @@ int launch_face_reduce(mh_system* s, const double* uhat, double* w, int rhs_mode
   FaceArgs a = make_args(s, uhat, w);
   if (s->t <= 16) return launch_small<16>(s, a, rhs_mode, pre);
   if (s->t <= 32) return launch_small<32>(s, a, rhs_mode, pre);
+  if (!rhs_mode && s->knobs.face_bulk) {
+    const size_t per = (size_t)(s->ldF + 128) * sizeof(double);
+    const int nw = (int)std::max<size_t>(1, std::min<size_t>(8, (size_t)(200 * 1024) / per));
+    const size_t smem = per * nw;
+    const int RTb = (s->t + 31) / 32;
+    const void* fn = nullptr;
+    if (RTb == 2) fn = pre ? (const void*)face_bulk_kernel<2, true> : (const void*)face_bulk_kernel<2, false>;
+    else if (RTb == 3) fn = pre ? (const void*)face_bulk_kernel<3, true> : (const void*)face_bulk_kernel<3, false>;
+    else if (RTb == 4) fn = pre ? (const void*)face_bulk_kernel<4, true> : (const void*)face_bulk_kernel<4, false>;
+    if (fn) {
+      const int per_sm = launch_occupancy(s->device, fn, nw * 32, smem);
+      if (per_sm < 0) return MH_E_CUDA;
+      const int64_t need = (s->F + nw - 1) / nw;
+      const unsigned grid = (unsigned)std::min<int64_t>(need, (int64_t)std::max(1, per_sm) * s->num_sms);
+      void* args[] = {(void*)&a};
+      MH_CHECK_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(nw * 32), args, smem, s->stream));
+      return MH_OK;
+    }
+  }
   const unsigned grid = (unsigned)((s->F + kFaceWarps - 1) / kFaceWarps);
   const size_t smem = (size_t)kFaceWarps * s->t * sizeof(double);
   const int RT = (s->t + 31) / 32;

@@ -79,6 +79,7 @@ struct Knobs {
   int mgs_small = 1;      // MEHDG_MGS_SMALL: the MGS block of a step as one kernel
   int mgs_ctas = 4;       // MEHDG_MGS_CTAS: its CTAs per SM (at most)
   int mgs_reg = 1;        // MEHDG_MGS_REG: w held in registers when it fits
+  int face_bulk = 1;      // MEHDG_FACE_BULK: TMA-staged face kernel for t > 32
   int gmres_graphs = 1;   // MEHDG_GMRES_GRAPHS: MGS block as a CUDA graph
   int64_t split_at = -1;  // MEHDG_SPLIT_AT: interior/halo macro split (-1: computed)
   void read();
@@ -120,6 +121,7 @@ struct mh_system {
   mh::DBuf<double> udiag;  // N*Q   diag(U)
   int64_t ldB = 0;         // per-macro stride of Bt / Cm (nc*Q rounded up to kStreamChunk)
   int64_t ldL = 0;         // per-macro stride of Lp / Up (Q(Q-1)/2 rounded up to kStreamChunk)
+  int64_t ldF = 0;         // per-face stride of D / Dinv (t*t rounded up to 16 bytes)
   mh::DBuf<double> dinv;   // N*Q   1/U_ii
   mh::DBuf<int32_t> piv;   // N*Q   LAPACK 0-based pivots
   mh::DBuf<int32_t> perm;  // N*Q   composed row permutation: (P x)_i = x[perm_i]
@@ -127,10 +129,10 @@ struct mh_system {
   mh::DBuf<double> Bt;     // N*nc*Q  op.B^T  (row c = column c of op.B)
   mh::DBuf<double> Cm;     // N*nc*Q  op.C    (aliases Bt when c_is_bt)
   mh::DBuf<double> Ru;     // N*Q
-  mh::DBuf<double> D;      // F*t*t  column-major face blocks
+  mh::DBuf<double> D;      // F*ldF  column-major face blocks
   mh::DBuf<double> Draw;   // F*t*t  row-major face blocks as uploaded (factor input)
   mh::DBuf<double> Rhat;   // F*t
-  mh::DBuf<double> Dinv;   // F*t*t  D_f^-1 column-major (sign folded in)
+  mh::DBuf<double> Dinv;   // F*ldF  D_f^-1 column-major (sign folded in)
   mh::DBuf<int8_t> Fkind;  // F
   mh::DBuf<double> V;      // (N*nfe + extra)*t  element slot contributions
   mh::DBuf<double> tmp;    // F*t scratch
