@@ -160,6 +160,31 @@ int halo_rhs_begin(mh_system* s) {
   return MH_OK;
 }
 
+// m values per rank summed over ranks in rank order (identically on every rank)
+__global__ void ordered_sum_vec(const double* __restrict__ parts, int nranks, int m,
+                                double* __restrict__ out) {
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    double s = 0.0;
+    for (int r = 0; r < nranks; ++r) s += parts[(size_t)r * m + i];
+    out[i] = s;
+  }
+}
+
+int allreduce_vec(mh_system* s, const double* local, int m, double* out) {
+  if (!multi(s)) {
+    ordered_sum_vec<<<1, 128, 0, s->stream>>>(local, 1, m, out);
+    MH_CHECK_CUDA(cudaGetLastError());
+    return MH_OK;
+  }
+  MH_CHECK(need_comm(s));
+  MH_CHECK(s->dot_all.ensure((size_t)s->nranks * m));
+  MH_CHECK_NCCL(g_nccl.AllGather(local, s->dot_all.p, (size_t)m, ncclFloat64,
+                                 (ncclComm_t)s->nccl, s->stream));
+  ordered_sum_vec<<<1, 128, 0, s->stream>>>(s->dot_all.p, s->nranks, m, out);
+  MH_CHECK_CUDA(cudaGetLastError());
+  return MH_OK;
+}
+
 int allreduce_scalar(mh_system* s, const double* local, double* out, bool take_sqrt) {
   if (!multi(s)) {
     ordered_sum<<<1, 32, 0, s->stream>>>(local, 1, take_sqrt, out);
@@ -167,7 +192,7 @@ int allreduce_scalar(mh_system* s, const double* local, double* out, bool take_s
     return MH_OK;
   }
   MH_CHECK(need_comm(s));
-  MH_CHECK(s->dot_all.alloc((size_t)s->nranks));
+  MH_CHECK(s->dot_all.ensure((size_t)s->nranks));
   MH_CHECK_NCCL(g_nccl.AllGather(local, s->dot_all.p, 1, ncclFloat64, (ncclComm_t)s->nccl,
                                  s->stream));
   ordered_sum<<<1, 32, 0, s->stream>>>(s->dot_all.p, s->nranks, take_sqrt, out);

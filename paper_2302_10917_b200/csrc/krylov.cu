@@ -45,6 +45,7 @@ struct Krylov {
   // device Arnoldi pipeline (pipelined solves): the Hessenberg matrix, the
   // rotations, g, the per-step residual estimates and the control block
   DBuf<double> Hd, csd, snd, gd, histd;
+  DBuf<double> cgs;          // CGS2: partials (2 x (restart+2) x dot_parts) and sums
   DBuf<int> ctl;             // GmresCtl
   int* ctl_host = nullptr;   // pinned, two slots of kCtlInts
   const int* skip = nullptr; // &ctl->stop while a pipelined cycle runs
@@ -89,6 +90,7 @@ struct Krylov {
     MH_CHECK(gd.alloc((size_t)restart + 1));
     MH_CHECK(histd.alloc((size_t)restart));
     MH_CHECK(ctl.alloc(8));
+    MH_CHECK(cgs.alloc((size_t)(restart + 2) * kDotPartsMax + 4 * ((size_t)restart + 2)));
     if (!ctl_host) MH_CHECK_CUDA(cudaMallocHost(&ctl_host, sizeof(int) * 16));
     return MH_OK;
   }
@@ -100,6 +102,7 @@ struct Krylov {
     V.release(); w.release(); tmp.release(); tmp2.release(); part.release();
     hcol.release(); ydev.release(); scal.release(); ticket.release(); bar.release();
     Hd.release(); csd.release(); snd.release(); gd.release(); histd.release(); ctl.release();
+    cgs.release();
     if (h_host) cudaFreeHost(h_host);
     if (ctl_host) cudaFreeHost(ctl_host);
   }
@@ -337,6 +340,74 @@ mgs_reg_kernel(int64_t n, const double* __restrict__ w, const double* __restrict
   }
 }
 
+// ---- the multi-rank Arnoldi step: classical Gram-Schmidt twice (CGS2) --
+// MGS needs k + 2 dependent reductions per step, i.e. k + 2 collectives on a
+// multi-rank system; CGS2 needs two: h = V^T w (one batched reduction of k + 2
+// values, the last being ||w||^2), w -= V h, then h2 = V^T w and ||w||^2 again,
+// w -= V h2; H[0..k, k] = h + h2 and ||w_final||^2 = ||w||^2 - ||h2||^2.  Each
+// batched reduction uses the dot partition (dot_parts(n) warp partials, fixed
+// order), the rank sums are all-gathered and added in rank order: every rank
+// holds identical values.  Within the solve tolerance of MGS, not bitwise.
+__global__ void __launch_bounds__(kDotWarps * 32)
+multidot_kernel(int64_t n, const double* __restrict__ V, int m, const double* __restrict__ w,
+                double* __restrict__ part, unsigned* __restrict__ ticket,
+                double* __restrict__ out, const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int b = blockIdx.x * kDotWarps + wp;
+  const int P = gridDim.x * kDotWarps;
+  const int64_t lo = n * b / P, hi = n * (b + 1) / P;
+  for (int i = 0; i <= m; ++i) {  // i < m: V_i . w; i == m: w . w
+    const double* y = i < m ? V + (size_t)i * n : w;
+    double acc = 0.0;
+#pragma unroll 4
+    for (int64_t j = lo + lane; j < hi; j += 32) acc = fma(w[j], y[j], acc);
+    acc = warp_xor_sum(acc);
+    if (lane == 0) part[(size_t)i * P + b] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned tk = atomicAdd(ticket, 1u);
+    last = (tk == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int i = wp; i <= m; i += kDotWarps) {
+    const double tot = parts_sum(part + (size_t)i * P, P, lane);
+    if (lane == 0) out[i] = tot;
+  }
+  if (threadIdx.x == 0) *ticket = 0u;
+}
+
+// w -= sum_i h[i] V_i (i ascending)
+__global__ void cgs_update_kernel(int64_t n, const double* __restrict__ V, int m,
+                                  const double* __restrict__ h, double* __restrict__ w,
+                                  const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    double x = w[j];
+    for (int i = 0; i < m; ++i) x = __dsub_rn(x, __dmul_rn(h[i], V[(size_t)i * n + j]));
+    w[j] = x;
+  }
+}
+
+// H[0..k, k] = h + h2; H[k+1, k] = sqrt(||w||^2 - ||h2||^2)
+__global__ void cgs_finalize_kernel(const double* __restrict__ h, const double* __restrict__ h2,
+                                    int k, double* __restrict__ hcol, const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  if (threadIdx.x != 0) return;
+  double q = 0.0;
+  for (int i = 0; i <= k; ++i) {
+    hcol[i] = h[i] + h2[i];
+    q = fma(h2[i], h2[i], q);
+  }
+  hcol[k + 1] = sqrt(fmax(h2[k + 1] - q, 0.0));
+}
+
 // V[k+1] = w / h if h > 1e-300 (else left zero: breakdown)
 __global__ void normalize_kernel(int64_t n, const double* __restrict__ w,
                                  const double* __restrict__ h, double* __restrict__ out,
@@ -556,6 +627,34 @@ int enqueue_mgs(cudaStream_t st, Krylov* K, int64_t n, int k, bool copy_host = t
   if (copy_host)
     MH_CHECK_CUDA(cudaMemcpyAsync(K->h_host, K->hcol.p, sizeof(double) * (k + 2),
                                   cudaMemcpyDeviceToHost, st));
+  return MH_OK;
+}
+
+// The multi-rank Arnoldi step (CGS2, two collectives): H[0..k+1, k] to hcol,
+// V[k+1] = w / H[k+1, k].
+int enqueue_cgs2(cudaStream_t st, Krylov* K, int64_t n, int k) {
+  double* V = K->V.p;
+  const int m = k + 1;
+  const int P = dot_parts(n);
+  double* part = K->cgs.p;
+  double* loc = part + (size_t)(K->restart + 2) * kDotPartsMax;
+  double* hA = loc + (K->restart + 2);
+  double* hB = hA + (K->restart + 2);
+  const dim3 vg(kVecGrid), vb(kVecThreads);
+  for (int pass = 0; pass < 2; ++pass) {
+    double* h = pass == 0 ? hA : hB;
+    multidot_kernel<<<P / kDotWarps, kDotWarps * 32, 0, st>>>(n, V, m, K->w.p, part, K->ticket.p,
+                                                            loc, K->skip);
+    MH_CHECK_CUDA(cudaGetLastError());
+    MH_CHECK(allreduce_vec(g_comm_sys, loc, m + 1, h));  // one collective
+    cgs_update_kernel<<<vg, vb, 0, st>>>(n, V, m, h, K->w.p, K->skip);
+    MH_CHECK_CUDA(cudaGetLastError());
+  }
+  cgs_finalize_kernel<<<1, 32, 0, st>>>(hA, hB, k, K->hcol.p, K->skip);
+  MH_CHECK_CUDA(cudaGetLastError());
+  normalize_kernel<<<vg, vb, 0, st>>>(n, K->w.p, K->hcol.p + k + 1, V + (size_t)(k + 1) * n,
+                                      K->skip);
+  MH_CHECK_CUDA(cudaGetLastError());
   return MH_OK;
 }
 
@@ -853,7 +952,8 @@ int gmres_pipelined(mh_system* s, cudaStream_t st, Krylov* K, int64_t n, const O
         if (tr.on) tr.mark(st, 0);
         MH_CHECK(apply_MA(A, M, MA, Vk, K->w.p, K->tmp.p));
         if (tr.on) tr.mark(st, 1);
-        if (use_graphs) MH_CHECK(run_mgs(st, K, n, k));
+        if (multi) MH_CHECK(enqueue_cgs2(st, K, n, k));  // two collectives per step
+        else if (use_graphs) MH_CHECK(run_mgs(st, K, n, k));
         else MH_CHECK(enqueue_mgs(st, K, n, k, false));
         if (tr.on) tr.mark(st, 2);
         givens_kernel<<<1, 32, 0, st>>>(K->hcol.p, K->Hd.p, K->csd.p, K->snd.p, K->gd.p,

@@ -58,6 +58,8 @@ struct DBuf {
     n = count;
     return MH_OK;
   }
+  // grow-only: keeps a buffer that enqueued work may still use when it is large enough
+  int ensure(size_t count) { return count <= n && p ? MH_OK : alloc(count); }
   void release() {
     if (p) cudaFree(p);
     p = nullptr;
@@ -202,4 +204,6 @@ int halo_rhs_begin(mh_system* s);
 void free_comm(mh_system* s);
 // sum a device scalar over ranks (rank order) into out; sqrt if requested
 int allreduce_scalar(mh_system* s, const double* local, double* out, bool take_sqrt);
+// m values per rank, each summed over ranks in rank order, into out[m] (device)
+int allreduce_vec(mh_system* s, const double* local, int m, double* out);
 }  // namespace mh

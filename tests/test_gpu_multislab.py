@@ -61,8 +61,8 @@ def test_single_rank_plan_matches_plain_system(gpu):
 @pytest.mark.parametrize("split", [None, 0, 37, 64])
 def test_single_rank_nccl_communicator(gpu, split, monkeypatch):
     """The NCCL path (dlopen, ncclCommInitRank, grouped halo calls, all-gathered
-    dot products, GMRES without graphs) on a one-rank communicator: bitwise the
-    plain single-GPU apply and solve.  `split` forces the interior / halo macro
+    batched reductions, GMRES with CGS2) on a one-rank communicator: bitwise the
+    plain single-GPU apply, the solve within tolerance.  `split` forces the interior / halo macro
     split of the apply (macros [split, N) on the second stream, overlapping the
     halo exchange; [0, split) after it)."""
     if split is not None:
@@ -78,9 +78,12 @@ def test_single_rank_nccl_communicator(gpu, split, monkeypatch):
     u = torch.as_tensor(prob["uhat"], device="cuda")
     assert torch.equal(rs.apply(u), P.apply_schur(ref, u))
     assert np.array_equal(rs.f_dev.cpu().numpy(), ref.f_vec)
+    # the multi-rank GMRES orthogonalises with CGS2 (two collectives per Arnoldi
+    # step, krylov.cu) instead of the reference's MGS: same solve within tolerance
     x, info = rs.gmres(tol=1e-10)
     xr, ir = P.gmres(P.SchurOperator(ref), ref.f_device, P.SolverConfig(tol=1e-10),
                      precond=P.Preconditioner(ref))
-    assert info["converged"] and info["iterations"] == ir["iterations"]
+    assert info["converged"] and abs(info["iterations"] - ir["iterations"]) <= 1
     xr = xr.cpu().numpy() if hasattr(xr, "cpu") else np.asarray(xr)
-    assert np.array_equal(x.cpu().numpy(), xr)
+    xn = x.cpu().numpy()
+    assert np.linalg.norm(xn - xr) <= 1e-9 * np.linalg.norm(xr)
