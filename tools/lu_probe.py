@@ -1,6 +1,6 @@
 """Time the batched LU alone on one config: python tools/lu_probe.py c2 [reps].
 
-MEHDG_LU=left|dmma|reg selects the kernel (see csrc/lu.cu launch_lu).  Used
+MEHDG_LU=tile|cta selects the kernel (see csrc/lu.cu launch_lu).  Used
 for kernel design points and as the ncu target for the LU."""
 import ctypes as C
 import os
