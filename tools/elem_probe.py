@@ -1,6 +1,6 @@
 """Time the matrix-free apply alone: python tools/elem_probe.py c3 [reps] [KNOB=v1,v2 ...].
 
-Knobs are environment variables read at each launch (MEHDG_ELEM_CTAS, ...).
+Knobs are environment variables read when a system is created (MEHDG_ELEM_CTAS, ...).
 Prints applies/s and the element kernel's algorithmic GB/s per setting."""
 import itertools
 import os
