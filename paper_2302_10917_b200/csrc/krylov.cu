@@ -166,9 +166,16 @@ __device__ __forceinline__ double dot_partial(int64_t n, int P, int b, double* _
 // published before a fence + barrier / ticket: L2-coherent loads (ld.cg, no
 // stale L1 line), issued together rather than one volatile load at a time
 __device__ __forceinline__ double parts_sum(const double* part, int P, int lane) {
+  // all of a lane's partials (<= kDotPartsMax / 32) in flight at once, then the
+  // fixed-order sum: one memory round trip instead of one per load
+  constexpr int kMax = kDotPartsMax / 32;
+  double x[kMax];
+#pragma unroll
+  for (int u = 0; u < kMax; ++u) x[u] = (lane + 32 * u < P) ? __ldcg(part + lane + 32 * u) : 0.0;
   double v = 0.0;
-#pragma unroll 8
-  for (int i = lane; i < P; i += 32) v += __ldcg(part + i);
+#pragma unroll
+  for (int u = 0; u < kMax; ++u)
+    if (lane + 32 * u < P) v += x[u];
   return warp_xor_sum(v);
 }
 
