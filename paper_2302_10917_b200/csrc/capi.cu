@@ -142,6 +142,8 @@ void Knobs::read() {
   if (const char* v = env("MEHDG_LU_APOL")) lu_a_pol = atoi(v);
   if (const char* v = env("MEHDG_ELEM_CTAS")) elem_ctas = std::max(0, atoi(v));
   if (const char* v = env("MEHDG_ELEM_CH")) elem_ch = atoi(v);
+  if (const char* v = env("MEHDG_ELEM_BPOL")) elem_bpol = atoi(v);
+  if (const char* v = env("MEHDG_ELEM_LPOL")) elem_lpol = atoi(v);
   if (const char* v = env("MEHDG_MGS_SMALL")) mgs_small = atoi(v);
   if (const char* v = env("MEHDG_MGS_CTAS")) mgs_ctas = std::max(1, atoi(v));
   if (const char* v = env("MEHDG_MGS_REG")) mgs_reg = atoi(v);

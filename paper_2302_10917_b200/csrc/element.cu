@@ -75,6 +75,7 @@ struct ElemArgs {
   int64_t e_lo;  // macros [e_lo, N) are processed
   int Q, nc, t, nfe;
   int c_is_bt;
+  int bpol, lpol;  // L2 policies of the op.B^T first read and of the L / U streams
   const int* skip;  // a stopped speculative GMRES step: return at once
 };
 
@@ -200,9 +201,9 @@ element_kernel(ElemArgs a) {
   (void)t;
   if (threadIdx.x == 0) {
     int n = 0;
-    if (MODE != kRhs) segs[n++] = Segment{a.Bt, a.ldB, nchB, (MODE == kApply && a.c_is_bt) ? 1 : 0};
-    segs[n++] = Segment{a.Lp, a.ldL, nchL, 0};
-    segs[n++] = Segment{a.Up, a.ldL, nchL, 0};
+    if (MODE != kRhs) segs[n++] = Segment{a.Bt, a.ldB, nchB, (MODE == kApply && a.c_is_bt) ? a.bpol : 0};
+    segs[n++] = Segment{a.Lp, a.ldL, nchL, a.lpol};
+    segs[n++] = Segment{a.Up, a.ldL, nchL, a.lpol};
     if (MODE != kRecon) segs[n++] = Segment{a.Cm, a.ldB, nchB, 0};
     for (int i = 0; i < 2 * kWPB * S; ++i) mbar_init(&full[i], 1);  // full + empty
     fence_mbar_init();
@@ -516,6 +517,8 @@ int launch_mode(mh_system* s, const double* uhat, double* out, cudaStream_t st, 
   a.t = s->t;
   a.nfe = s->nfe;
   a.c_is_bt = s->c_is_bt ? 1 : 0;
+  a.bpol = s->knobs.elem_bpol;
+  a.lpol = s->knobs.elem_lpol;
   a.skip = MODE == kApply ? s->skip : nullptr;
   switch ((s->Q + 31) / 32) {
     case 1: return launch_rm<1, MODE>(s, a, st);

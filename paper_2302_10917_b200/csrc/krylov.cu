@@ -35,6 +35,20 @@ __host__ __device__ inline int dot_parts(int64_t n) {
   return p;
 }
 
+// The Givens state of a pipelined solve (device pointers and the solve's
+// constants, themselves in device memory so that a captured graph stays valid
+// from solve to solve): par = {bnorm, tol, maxiter}.
+struct GivensDev {
+  double* H;
+  double* cs;
+  double* sn;
+  double* g;
+  double* hist;
+  int* ctl;
+  const double* par;
+  int m;
+};
+
 struct Krylov {
   int64_t n = 0;
   int restart = 0;
@@ -47,7 +61,9 @@ struct Krylov {
   DBuf<double> Hd, csd, snd, gd, histd;
   DBuf<double> cgs;          // CGS2: partials (2 x (restart+2) x dot_parts) and sums
   DBuf<int> ctl;             // GmresCtl
-  int* ctl_host = nullptr;   // pinned, two slots of kCtlInts
+  DBuf<double> gpar;         // {bnorm, tol, maxiter} of the running solve
+  DBuf<GivensDev> gvd;       // the device copy of the Givens state (fused MGS tail)
+  int* ctl_host = nullptr;   // pinned: two slots of kCtlInts, then 4 doubles (the solve constants)
   const int* skip = nullptr; // &ctl->stop while a pipelined cycle runs
   bool persistent = false;   // a system's workspace, reused across solves
   // CUDA graphs of the Arnoldi step's MGS block, one per basis size k (captured
@@ -90,8 +106,14 @@ struct Krylov {
     MH_CHECK(gd.alloc((size_t)restart + 1));
     MH_CHECK(histd.alloc((size_t)restart));
     MH_CHECK(ctl.alloc(8));
+    MH_CHECK(gpar.alloc(4));
+    MH_CHECK(gvd.alloc(1));
+    {
+      GivensDev gh{Hd.p, csd.p, snd.p, gd.p, histd.p, ctl.p, gpar.p, restart};
+      MH_CHECK_CUDA(cudaMemcpy(gvd.p, &gh, sizeof(gh), cudaMemcpyHostToDevice));
+    }
     MH_CHECK(cgs.alloc((size_t)(restart + 2) * kDotPartsMax + 4 * ((size_t)restart + 2)));
-    if (!ctl_host) MH_CHECK_CUDA(cudaMallocHost(&ctl_host, sizeof(int) * 16));
+    if (!ctl_host) MH_CHECK_CUDA(cudaMallocHost(&ctl_host, sizeof(int) * 16 + sizeof(double) * 4));
     return MH_OK;
   }
   ~Krylov() {
@@ -102,7 +124,7 @@ struct Krylov {
     V.release(); w.release(); tmp.release(); tmp2.release(); part.release();
     hcol.release(); ydev.release(); scal.release(); ticket.release(); bar.release();
     Hd.release(); csd.release(); snd.release(); gd.release(); histd.release(); ctl.release();
-    cgs.release();
+    cgs.release(); gpar.release(); gvd.release();
     if (h_host) cudaFreeHost(h_host);
     if (ctl_host) cudaFreeHost(ctl_host);
   }
@@ -179,6 +201,33 @@ __device__ __forceinline__ double parts_sum(const double* part, int P, int lane)
   return warp_xor_sum(v);
 }
 
+// The same total by a whole 8-warp CTA: warp g sums the g-th eighth of the
+// partials (lane l adds its partials l, l + 32, ... in order, then the xor tree),
+// the eight group sums are added in order.  At most 8 loads per lane, one memory
+// round trip; every thread returns the total.  THE dot-product value of the
+// single-rank kernels (dot_kernel, mgs_kernel, mgs_reg_kernel all end here).
+// sg: 8 doubles of shared memory, free again after the caller's next barrier.
+__device__ __forceinline__ double parts_sum_cta(const double* part, int P, double* sg, int lane,
+                                                int wp) {
+  constexpr int kMax = kDotPartsMax / 8 / 32;
+  const int per = P >> 3;  // P is a power of two >= 32
+  const double* pg = part + wp * per;
+  double x[kMax];
+#pragma unroll
+  for (int u = 0; u < kMax; ++u) x[u] = (lane + 32 * u < per) ? __ldcg(pg + lane + 32 * u) : 0.0;
+  double v = 0.0;
+#pragma unroll
+  for (int u = 0; u < kMax; ++u)
+    if (lane + 32 * u < per) v += x[u];
+  v = warp_xor_sum(v);
+  if (lane == 0) sg[wp] = v;
+  __syncthreads();
+  double t = sg[0];
+#pragma unroll
+  for (int g = 1; g < 8; ++g) t += sg[g];
+  return t;
+}
+
 // Fused MGS step.  mode 0: plain dot(x, y); mode 1: w -= c*Vp then dot(Vi, w);
 // mode 2: w -= c*Vp then dot(w, w) and out <- sqrt.  Result to *out (device).
 // A set *skip (a stopped speculative GMRES step) makes it a no-op.
@@ -189,6 +238,7 @@ dot_kernel(int64_t n, double* __restrict__ w, const double* __restrict__ Vp,
            double* __restrict__ out, const int* __restrict__ skip) {
   if (skip && *skip) return;
   __shared__ bool last;
+  __shared__ double sg[8];
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   const int b = blockIdx.x * kDotWarps + wp;
   const int P = gridDim.x * kDotWarps;
@@ -203,10 +253,10 @@ dot_kernel(int64_t n, double* __restrict__ w, const double* __restrict__ Vp,
     last = (tk == gridDim.x - 1);
   }
   __syncthreads();
-  if (!last || wp != 0) return;
+  if (!last) return;
   __threadfence();
-  const double tot = parts_sum(part, P, lane);
-  if (lane == 0) {
+  const double tot = parts_sum_cta(part, P, sg, lane, wp);
+  if (threadIdx.x == 0) {
     *out = (mode == 2 && take_sqrt) ? sqrt(tot) : tot;
     *ticket = 0u;
   }
@@ -222,33 +272,113 @@ dot_kernel(int64_t n, double* __restrict__ w, const double* __restrict__ Vp,
 constexpr int kMgsThreads = 256;
 
 
-__device__ __forceinline__ void grid_barrier(unsigned* count, volatile unsigned* gen) {
+// Control block of a pipelined GMRES cycle (device ints)
+enum GmresCtl { kStop = 0, kKUsed = 1, kIt = 2, kConv = 3, kBreak = 4, kSteps = 5 };
+constexpr int kCtlInts = 8;
+constexpr int kMaxRestartSmem = 1024;  // restart lengths the device Givens supports
+
+// Step k's Givens update, one warp, the reference's arithmetic
+// (schur_solver.py:351-375): the new Hessenberg column, the previous rotations,
+// the new rotation, g, the residual estimate and the stopping rules.  Once a
+// cycle stops (converged, breakdown, maxiter) every later step of it is a no-op
+// -- the host enqueues steps ahead without waiting for each one.
+// sh / sc / ss: kMaxRestartSmem (+2) doubles of shared memory each.
+__device__ __forceinline__ void givens_step(const double* hcol, const GivensDev& G, int k,
+                                            double* sh, double* sc, double* ss, int lane) {
+  if (G.ctl[kStop]) return;
+  const int m = G.m;
+  const double bnorm = G.par[0], tol = G.par[1];
+  const int maxiter = (int)G.par[2];
+  for (int i = lane; i <= k + 1; i += 32) sh[i] = __ldcg(hcol + i);
+  for (int i = lane; i < k; i += 32) {
+    sc[i] = G.cs[i];
+    ss[i] = G.sn[i];
+  }
+  __syncwarp();
+  if (lane == 0) {
+    const bool breakdown = !(sh[k + 1] > 1e-300);
+    for (int i = 0; i < k; ++i) {
+      const double tt = sc[i] * sh[i] + ss[i] * sh[i + 1];
+      sh[i + 1] = -ss[i] * sh[i] + sc[i] * sh[i + 1];
+      sh[i] = tt;
+    }
+    const double denom = hypot(sh[k], sh[k + 1]);
+    if (denom == 0.0) {
+      G.ctl[kKUsed] = k + 1;
+      G.ctl[kBreak] = 1;
+      G.ctl[kStop] = 1;
+    } else {
+      const double c = sh[k] / denom, sgn = sh[k + 1] / denom;
+      G.cs[k] = c;
+      G.sn[k] = sgn;
+      sh[k] = denom;
+      sh[k + 1] = 0.0;
+      const double gk = G.g[k];
+      G.g[k + 1] = -sgn * gk;
+      G.g[k] = c * gk;
+      const int it = ++G.ctl[kIt];
+      const double res = fabs(G.g[k + 1]);
+      G.hist[G.ctl[kSteps]++] = res;
+      G.ctl[kKUsed] = k + 1;
+      if (res / bnorm <= tol) {
+        G.ctl[kConv] = 1;
+        G.ctl[kStop] = 1;
+      } else if (breakdown || it >= maxiter) {
+        G.ctl[kBreak] = breakdown ? 1 : 0;
+        G.ctl[kStop] = 1;
+      }
+    }
+  }
+  __syncwarp();
+  for (int i = lane; i <= k + 1; i += 32) G.H[(size_t)i * m + k] = sh[i];
+}
+
+// Grid-wide barrier of a cooperative launch on ONE monotonic counter: barrier b
+// of a launch is passed once the counter reaches base + (b + 1) G, base being
+// the counter's value when the launch started (a multiple of G: read by every
+// CTA before its own first arrival, when at most G - 1 others have arrived,
+// and rounded down).  One fire-and-forget increment and one polled line per
+// barrier -- no second atomic by the last arriver.  The counter is zeroed at
+// the start of every solve; all launches of a solve use the same grid.
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void grid_barrier(unsigned* count, unsigned target) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    const unsigned g0 = *gen;
-    __threadfence();
-    if (atomicAdd(count, 1u) == gridDim.x - 1) {
-      *count = 0u;
-      __threadfence();
-      atomicAdd(const_cast<unsigned*>(gen), 1u);
-    } else {
-      while (*gen == g0) __nanosleep(64);  // back off: one L2 line polled by every CTA
+    __threadfence();  // this CTA's partials before its arrival
+    atomicAdd(count, 1u);
+    while ((int)(ld_acquire_u32(count) - target) < 0) {
     }
-    __threadfence();
   }
   __syncthreads();
+}
+
+__device__ __forceinline__ unsigned barrier_base(const unsigned* count, unsigned* sbase) {
+  if (threadIdx.x == 0) {
+    const unsigned v = ld_acquire_u32(count);
+    *sbase = v - v % gridDim.x;
+  }
+  __syncthreads();
+  return *sbase;
 }
 
 __global__ void __launch_bounds__(kMgsThreads)
 mgs_kernel(int64_t n, double* __restrict__ w, const double* __restrict__ V, int k,
            double* __restrict__ hcol, double* __restrict__ vnext, double* __restrict__ part2,
-           unsigned* __restrict__ bar, const int* __restrict__ skip) {
+           unsigned* __restrict__ bar, const int* __restrict__ skip, const GivensDev* gv) {
   if (skip && *skip) return;
-  __shared__ double hs;
+  __shared__ double sg[8];
+  __shared__ unsigned sbase;
+  __shared__ double gsh[kMaxRestartSmem + 2], gsc[kMaxRestartSmem], gss[kMaxRestartSmem];
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   const int WB = kMgsThreads / 32;
   const int gw = blockIdx.x * WB + wp, nw = gridDim.x * WB;
   const int P = dot_parts(n);
+  const unsigned base = gridDim.x > 1 ? barrier_base(bar, &sbase) : 0u;
   double c = 0.0;
   const double* Vp = nullptr;
   for (int i = 0; i <= k + 1; ++i) {
@@ -259,19 +389,17 @@ mgs_kernel(int64_t n, double* __restrict__ w, const double* __restrict__ V, int 
       const double pv = dot_partial(n, P, b, w, Vp, c, i > 0, Vi, mode, lane);
       if (lane == 0) part[b] = pv;
     }
-    if (gridDim.x > 1) grid_barrier(bar, bar + 1);
+    if (gridDim.x > 1) grid_barrier(bar, base + (unsigned)(i + 1) * gridDim.x);
     else __syncthreads();
-    if (wp == 0) {
-      double h = parts_sum(part, P, lane);
-      if (i == k + 1) h = sqrt(h);
-      if (lane == 0) {
-        hs = h;
-        if (blockIdx.x == 0) hcol[i] = h;
-      }
-    }
-    __syncthreads();
-    c = hs;
+    double h = parts_sum_cta(part, P, sg, lane, wp);
+    if (i == k + 1) h = sqrt(h);
+    if (blockIdx.x == 0 && threadIdx.x == 0) hcol[i] = h;
+    c = h;
     Vp = Vi;
+  }
+  if (gv && blockIdx.x == 0 && wp == 0) {
+    __syncwarp();
+    givens_step(hcol, *gv, k, gsh, gsc, gss, lane);
   }
   if (!(c > 1e-300)) return;
   for (int64_t j = blockIdx.x * (int64_t)kMgsThreads + threadIdx.x; j < n;
@@ -281,42 +409,41 @@ mgs_kernel(int64_t n, double* __restrict__ w, const double* __restrict__ V, int 
 
 // The same MGS block with w and the previous basis vector held in registers
 // (a warp per partial, at most E elements per lane): each reduction reads one
-// basis vector from memory and nothing is written until V[k+1] = w / ||w||.
-// Per element the operations and their order are dot_partial's, so the
-// results are bitwise those of mgs_kernel / dot_kernel.
+// basis vector from memory -- the next one is loaded BEFORE the barrier of the
+// current reduction, so its latency hides behind the barrier -- and nothing is
+// written until V[k+1] = w / ||w||.  Per element the operations and their
+// order are dot_partial's, so the results are bitwise those of mgs_kernel /
+// dot_kernel.
 template <int E>
-__global__ void __launch_bounds__(kMgsThreads)
+__global__ void __launch_bounds__(kMgsThreads, E <= 12 ? 2 : 1)
 mgs_reg_kernel(int64_t n, const double* __restrict__ w, const double* __restrict__ V, int k,
                double* __restrict__ hcol, double* __restrict__ vnext,
                double* __restrict__ part2, unsigned* __restrict__ bar,
-               const int* __restrict__ skip) {
+               const int* __restrict__ skip, const GivensDev* gv) {
   if (skip && *skip) return;
-  __shared__ double hs;
+  __shared__ double sg[8];
+  __shared__ unsigned sbase;
+  __shared__ double gsh[kMaxRestartSmem + 2], gsc[kMaxRestartSmem], gss[kMaxRestartSmem];
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   const int b = blockIdx.x * (kMgsThreads / 32) + wp;
   const int P = dot_parts(n);
   const int64_t lo = b < P ? n * b / P : 0, hi = b < P ? n * (b + 1) / P : 0;
-  double wr[E], vp[E];
+  const int cnt = (int)(hi - lo) - lane;  // element e of this lane is valid when 32 e < cnt
+  const unsigned base = barrier_base(bar, &sbase);
+  const double* vcur = V + lo + lane;
+  double wr[E], vp[E], yv[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) {
-    const int64_t j = lo + lane + 32 * e;
-    wr[e] = j < hi ? w[j] : 0.0;
+    wr[e] = 32 * e < cnt ? w[lo + lane + 32 * e] : 0.0;
+    yv[e] = 32 * e < cnt ? vcur[32 * e] : 0.0;  // V_0
     vp[e] = 0.0;
   }
   double c = 0.0;
   for (int i = 0; i <= k + 1; ++i) {
-    const double* Vi = V + (size_t)i * n;
-    double yv[E];
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const int64_t j = lo + lane + 32 * e;
-      yv[e] = (i <= k && j < hi) ? Vi[j] : 0.0;
-    }
     double acc = 0.0;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-      const int64_t j = lo + lane + 32 * e;
-      if (j < hi) {
+      if (32 * e < cnt) {
         double wi = wr[e];
         if (i > 0) wi = __dsub_rn(wi, __dmul_rn(c, vp[e]));
         wr[e] = wi;
@@ -324,27 +451,29 @@ mgs_reg_kernel(int64_t n, const double* __restrict__ w, const double* __restrict
       }
       vp[e] = yv[e];
     }
+    if (i + 1 <= k) {  // the next basis vector, in flight across the barrier
+      vcur += n;
+#pragma unroll
+      for (int e = 0; e < E; ++e) yv[e] = 32 * e < cnt ? vcur[32 * e] : 0.0;
+    }
     acc = warp_xor_sum(acc);
     double* part = part2 + (i & 1) * kDotPartsMax;
     if (lane == 0 && b < P) part[b] = acc;
-    grid_barrier(bar, bar + 1);
-    if (wp == 0) {
-      double h = parts_sum(part, P, lane);
-      if (i == k + 1) h = sqrt(h);
-      if (lane == 0) {
-        hs = h;
-        if (blockIdx.x == 0) hcol[i] = h;
-      }
-    }
-    __syncthreads();
-    c = hs;
+    grid_barrier(bar, base + (unsigned)(i + 1) * gridDim.x);
+    double h = parts_sum_cta(part, P, sg, lane, wp);
+    if (i == k + 1) h = sqrt(h);
+    if (blockIdx.x == 0 && threadIdx.x == 0) hcol[i] = h;
+    c = h;
+  }
+  if (gv && blockIdx.x == 0 && wp == 0) {
+    __syncwarp();
+    givens_step(hcol, *gv, k, gsh, gsc, gss, lane);
   }
   if (!(c > 1e-300)) return;
+  double* vn = vnext + lo + lane;
 #pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int64_t j = lo + lane + 32 * e;
-    if (j < hi) vnext[j] = wr[e] / c;
-  }
+  for (int e = 0; e < E; ++e)
+    if (32 * e < cnt) vn[32 * e] = wr[e] / c;
 }
 
 // ---- the multi-rank Arnoldi step: classical Gram-Schmidt twice (CGS2) --
@@ -427,66 +556,11 @@ __global__ void normalize_kernel(int64_t n, const double* __restrict__ w,
     out[i] = w[i] / hv;
 }
 
-// Control block of a pipelined GMRES cycle (device ints)
-enum GmresCtl { kStop = 0, kKUsed = 1, kIt = 2, kConv = 3, kBreak = 4, kSteps = 5 };
-constexpr int kCtlInts = 8;
-constexpr int kMaxRestartSmem = 1024;  // restart lengths the device Givens supports
-
-// Step k's Givens update on the device, the reference's arithmetic
-// (schur_solver.py:351-375): the new Hessenberg column, the previous rotations,
-// the new rotation, g, the residual estimate and the stopping rules.  Once a
-// cycle stops (converged, breakdown, maxiter) every later step of it is a no-op
-// -- the host enqueues steps ahead without waiting for each one.
-__global__ void givens_kernel(const double* __restrict__ hcol, double* __restrict__ H,
-                              double* __restrict__ cs, double* __restrict__ sn,
-                              double* __restrict__ g, double* __restrict__ hist,
-                              int* __restrict__ ctl, int k, int m, double bnorm, double tol,
-                              int maxiter) {
+// Step k's Givens update as its own launch (multi-rank CGS2 steps and the
+// MGS block as separate launches; the one-launch MGS block does it in its tail)
+__global__ void givens_kernel(const double* __restrict__ hcol, GivensDev G, int k) {
   __shared__ double sh[kMaxRestartSmem + 2], sc[kMaxRestartSmem], ss[kMaxRestartSmem];
-  if (ctl[kStop]) return;
-  const int lane = threadIdx.x;
-  for (int i = lane; i <= k + 1; i += 32) sh[i] = hcol[i];
-  for (int i = lane; i < k; i += 32) {
-    sc[i] = cs[i];
-    ss[i] = sn[i];
-  }
-  __syncwarp();
-  if (lane == 0) {
-    const bool breakdown = !(sh[k + 1] > 1e-300);
-    for (int i = 0; i < k; ++i) {
-      const double tt = sc[i] * sh[i] + ss[i] * sh[i + 1];
-      sh[i + 1] = -ss[i] * sh[i] + sc[i] * sh[i + 1];
-      sh[i] = tt;
-    }
-    const double denom = hypot(sh[k], sh[k + 1]);
-    if (denom == 0.0) {
-      ctl[kKUsed] = k + 1;
-      ctl[kBreak] = 1;
-      ctl[kStop] = 1;
-    } else {
-      const double c = sh[k] / denom, sgn = sh[k + 1] / denom;
-      cs[k] = c;
-      sn[k] = sgn;
-      sh[k] = denom;
-      sh[k + 1] = 0.0;
-      const double gk = g[k];
-      g[k + 1] = -sgn * gk;
-      g[k] = c * gk;
-      const int it = ++ctl[kIt];
-      const double res = fabs(g[k + 1]);
-      hist[ctl[kSteps]++] = res;
-      ctl[kKUsed] = k + 1;
-      if (res / bnorm <= tol) {
-        ctl[kConv] = 1;
-        ctl[kStop] = 1;
-      } else if (breakdown || it >= maxiter) {
-        ctl[kBreak] = breakdown ? 1 : 0;
-        ctl[kStop] = 1;
-      }
-    }
-  }
-  __syncwarp();
-  for (int i = lane; i <= k + 1; i += 32) H[(size_t)i * m + k] = sh[i];
+  givens_step(hcol, G, k, sh, sc, ss, threadIdx.x);
 }
 
 __global__ void scale_kernel(int64_t n, const double* __restrict__ x, double inv_div,
@@ -579,7 +653,15 @@ int gmres_core(cudaStream_t st, Krylov* K, int64_t n, const OpFn& A, const OpFn&
 
 // The MGS block of Arnoldi step k: H[0..k, k] and H[k+1, k] = ||w||, V[k+1] = w / H[k+1, k],
 // and the new Hessenberg column copied to the pinned host buffer.
-int enqueue_mgs(cudaStream_t st, Krylov* K, int64_t n, int k, bool copy_host = true) {
+// True when the MGS block of a step is ONE launch (which can then run the
+// step's Givens update in its tail).
+bool mgs_one_launch() {
+  const bool multi = g_comm_sys && (g_comm_sys->nranks > 1 || g_comm_sys->nccl);
+  return !multi && proc_knobs().mgs_small;
+}
+
+int enqueue_mgs(cudaStream_t st, Krylov* K, int64_t n, int k, bool copy_host = true,
+                bool fuse_givens = false) {
   double* V = K->V.p;
   const bool multi = g_comm_sys && (g_comm_sys->nranks > 1 || g_comm_sys->nccl);
   if (!multi && proc_knobs().mgs_small) {
@@ -593,7 +675,9 @@ int enqueue_mgs(cudaStream_t st, Krylov* K, int64_t n, int k, bool copy_host = t
     if (proc_knobs().mgs_reg && per_lane <= 16) {
       const void* fr = per_lane <= 4 ? (const void*)mgs_reg_kernel<4>
                        : per_lane <= 8 ? (const void*)mgs_reg_kernel<8>
-                                       : (const void*)mgs_reg_kernel<16>;
+                       : per_lane <= 10 ? (const void*)mgs_reg_kernel<10>
+                       : per_lane <= 12 ? (const void*)mgs_reg_kernel<12>
+                                        : (const void*)mgs_reg_kernel<16>;
       int dev = 0;
       MH_CHECK_CUDA(cudaGetDevice(&dev));
       const int per_sm = launch_occupancy(dev, fr, kMgsThreads, 0);
@@ -603,8 +687,10 @@ int enqueue_mgs(cudaStream_t st, Krylov* K, int64_t n, int k, bool copy_host = t
       }
     }
     double* vnext = V + (size_t)(k + 1) * n;
+    const GivensDev* gv = fuse_givens ? K->gvd.p : nullptr;
     void* args[] = {(void*)&n, (void*)&K->w.p, (void*)&V, (void*)&k, (void*)&K->hcol.p,
-                    (void*)&vnext, (void*)&K->part.p, (void*)&K->bar.p, (void*)&K->skip};
+                    (void*)&vnext, (void*)&K->part.p, (void*)&K->bar.p, (void*)&K->skip,
+                    (void*)&gv};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(G);
     cfg.blockDim = dim3(kMgsThreads);
@@ -680,7 +766,7 @@ int run_mgs(cudaStream_t st, Krylov* K, int64_t n, int k) {
   if (!K->mgs[k]) {
     cudaGraph_t g = nullptr;
     MH_CHECK_CUDA(cudaStreamBeginCapture(K->gs, cudaStreamCaptureModeThreadLocal));
-    const int st_enq = enqueue_mgs(K->gs, K, n, k, false);
+    const int st_enq = enqueue_mgs(K->gs, K, n, k, false, true);
     const cudaError_t ce = cudaStreamEndCapture(K->gs, &g);
     MH_CHECK(st_enq);
     MH_CHECK_CUDA(ce);
@@ -702,6 +788,7 @@ int gmres_core(cudaStream_t st, Krylov* K, int64_t n, const OpFn& A, const OpFn&
                int* hist_len) {
   std::vector<double> history;
   MH_CHECK_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, st));
+  MH_CHECK_CUDA(cudaMemsetAsync(K->bar.p, 0, 2 * sizeof(unsigned), st));
   // bnorm = ||M b||
   const double* mb = rhs;
   if (M.fn) {
@@ -842,6 +929,7 @@ int gmres_pipelined(mh_system* s, cudaStream_t st, Krylov* K, int64_t n, const O
                     double* hist_host, int hist_cap, int* hist_len) {
   std::vector<double> history;
   MH_CHECK_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, st));
+  MH_CHECK_CUDA(cudaMemsetAsync(K->bar.p, 0, 2 * sizeof(unsigned), st));
   const double* mb = rhs;
   if (M.fn) {
     MH_CHECK(M(rhs, K->tmp.p));
@@ -868,6 +956,15 @@ int gmres_pipelined(mh_system* s, cudaStream_t st, Krylov* K, int64_t n, const O
   const int m = restart;
   const bool multi = g_comm_sys && (g_comm_sys->nranks > 1 || g_comm_sys->nccl);
   const bool use_graphs = !multi && proc_knobs().gmres_graphs;
+  const bool fused = mgs_one_launch();  // the Givens update in the MGS launch's tail
+  const GivensDev gvh{K->Hd.p, K->csd.p, K->snd.p, K->gd.p, K->histd.p, K->ctl.p, K->gpar.p, m};
+  {
+    double* par = reinterpret_cast<double*>(K->ctl_host + 16);  // pinned, written once per solve
+    par[0] = bnorm;
+    par[1] = tol;
+    par[2] = (double)maxiter;
+    MH_CHECK_CUDA(cudaMemcpyAsync(K->gpar.p, par, 3 * sizeof(double), cudaMemcpyHostToDevice, st));
+  }
   std::vector<double> H((size_t)(m + 1) * m), g(m + 1), y(m), hist(m);
   auto Hat = [&](int i, int k) -> double& { return H[(size_t)i * m + k]; };
   double* V = K->V.p;
@@ -926,9 +1023,12 @@ int gmres_pipelined(mh_system* s, cudaStream_t st, Krylov* K, int64_t n, const O
         r = K->w.p;
       }
     }
-    MH_CHECK(dot_dev(st, K, n, r, nullptr, nullptr, nullptr, 2, K->scal.p));
-    MH_CHECK(read_scalars(st, K, K->scal.p, 1));
-    const double beta = K->h_host[0];
+    double beta = bnorm;  // x = 0: r = M b, whose norm is bnorm (the same reduction)
+    if (!x_zero) {
+      MH_CHECK(dot_dev(st, K, n, r, nullptr, nullptr, nullptr, 2, K->scal.p));
+      MH_CHECK(read_scalars(st, K, K->scal.p, 1));
+      beta = K->h_host[0];
+    }
     if (history.empty()) history.push_back(beta);
     if (beta / bnorm <= tol) {
       conv = true;
@@ -947,7 +1047,9 @@ int gmres_pipelined(mh_system* s, cudaStream_t st, Krylov* K, int64_t n, const O
     MH_CHECK_CUDA(cudaMemcpyAsync(K->ctl.p, ch, sizeof(int) * kCtlInts, cudaMemcpyHostToDevice, st));
     scale_kernel<<<vg, vb, 0, st>>>(n, r, beta, V);
     MH_CHECK_CUDA(cudaGetLastError());
-    MH_CHECK_CUDA(cudaStreamSynchronize(st));  // pinned buffers reused below
+    // no host wait here: h_host[0] and ch[0..8) are next written by the host after
+    // the cycle's final synchronize, and the chunk read-backs into ch are ordered
+    // after the upload on the stream
     K->skip = K->ctl.p + kStop;
     s->skip = K->skip;
     int k = 0, chunk = 0;
@@ -961,11 +1063,12 @@ int gmres_pipelined(mh_system* s, cudaStream_t st, Krylov* K, int64_t n, const O
         if (tr.on) tr.mark(st, 1);
         if (multi) MH_CHECK(enqueue_cgs2(st, K, n, k));  // two collectives per step
         else if (use_graphs) MH_CHECK(run_mgs(st, K, n, k));
-        else MH_CHECK(enqueue_mgs(st, K, n, k, false));
+        else MH_CHECK(enqueue_mgs(st, K, n, k, false, fused));
         if (tr.on) tr.mark(st, 2);
-        givens_kernel<<<1, 32, 0, st>>>(K->hcol.p, K->Hd.p, K->csd.p, K->snd.p, K->gd.p,
-                                       K->histd.p, K->ctl.p, k, m, bnorm, tol, maxiter);
-        MH_CHECK_CUDA(cudaGetLastError());
+        if (!fused) {
+          givens_kernel<<<1, 32, 0, st>>>(K->hcol.p, gvh, k);
+          MH_CHECK_CUDA(cudaGetLastError());
+        }
         if (tr.on) tr.mark(st, 3);
       }
       const int slot = chunk & 1;

@@ -78,6 +78,8 @@ struct Knobs {
   int lu_a_pol = 1;       // MEHDG_LU_APOL: L2 policy of the A stream (1 evict_first)
   int elem_ctas = 0;      // MEHDG_ELEM_CTAS: cap on element-kernel CTAs per SM (0: none)
   int elem_ch = 512;      // MEHDG_ELEM_CH: element stream chunk (doubles)
+  int elem_bpol = 1;      // MEHDG_ELEM_BPOL: L2 policy of op.B^T's first read when it is re-read (0 evict_first, 1 evict_last, 2 normal, 3 half evict_last)
+  int elem_lpol = 0;      // MEHDG_ELEM_LPOL: L2 policy of the L / U streams (0 evict_first, 2 normal)
   int mgs_small = 1;      // MEHDG_MGS_SMALL: the MGS block of a step as one kernel
   int mgs_ctas = 4;       // MEHDG_MGS_CTAS: its CTAs per SM (at most)
   int mgs_reg = 1;        // MEHDG_MGS_REG: w held in registers when it fits

@@ -68,6 +68,22 @@ __device__ __forceinline__ uint64_t l2_policy_evict_last() {
   asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+__device__ __forceinline__ uint64_t l2_policy_evict_normal() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last_half() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.L2::evict_first.b64 %0, 0.5;" : "=l"(p));
+  return p;
+}
+// segment policy: 0 evict_first, 1 evict_last, 2 normal, 3 evict_last on half the lines
+__device__ __forceinline__ uint64_t l2_policy(int keep) {
+  return keep == 1 ? l2_policy_evict_last()
+         : keep == 2 ? l2_policy_evict_normal()
+         : keep == 3 ? l2_policy_evict_last_half() : l2_policy_evict_first();
+}
 
 __device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
@@ -95,7 +111,7 @@ struct Segment {
   const double* base;  // segment of macro e starts at base + e * stride
   int64_t stride;      // doubles between consecutive macros (multiple of CH)
   int nch;             // chunks in the segment
-  int keep;            // 1: L2 evict_last (re-read soon), 0: evict_first
+  int keep;            // L2 policy: 0 evict_first, 1 evict_last (re-read soon), 2 normal, 3 half evict_last
 };
 
 // Warp-specialised ring pipeline: a producer warp of the CTA owns the
@@ -114,8 +130,6 @@ struct Pipe {
   static __device__ void produce(double* rings, uint64_t* full, uint64_t* empty,
                                  const Segment* seg, int nseg, int64_t warp0, int64_t W,
                                  int64_t nmacro, int ncons) {
-    const uint64_t pol_first = l2_policy_evict_first();
-    const uint64_t pol_last = l2_policy_evict_last();
     int per = 0;
     for (int s = 0; s < nseg; ++s) per += seg[s].nch;
     int first_seg = 0;
@@ -136,7 +150,7 @@ struct Pipe {
       if (first_seg < nseg) {
         src[w] = seg[first_seg].base + e0 * seg[first_seg].stride;
         rem[w] = seg[first_seg].nch;
-        pol[w] = seg[first_seg].keep ? pol_last : pol_first;
+        pol[w] = l2_policy(seg[first_seg].keep);
       }
     }
     // Round-robin over the consumer rings, one chunk per ring per round,
@@ -168,7 +182,7 @@ struct Pipe {
           const Segment& sg = seg[ps[w]];
           src[w] = sg.base + pe[w] * sg.stride;
           rem[w] = sg.nch;
-          pol[w] = sg.keep ? pol_last : pol_first;
+          pol[w] = l2_policy(sg.keep);
         }
       }
       if (!any) break;
