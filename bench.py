@@ -468,6 +468,13 @@ def run_ours(args, world, rank, local):
         P.form_element_schur(sys_)
         torch.cuda.synchronize(dev)
         t_form = time.perf_counter() - t0
+        e0.record(stream)  # the form kernel alone (S already allocated)
+        P.form_element_schur(sys_)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        form_ms = e0.elapsed_time(e1)
+        # two triangular solves with nc right-hand sides + the C Y product
+        form_flops = N * (2.0 * Q * Q * nc + 2.0 * nc * nc * Q)
         for _ in range(3):
             check(lib.mh_apply_mb(h, ptr(u), ptr(w)), "apply_mb")
         mb_steps = max(10, args.steps // 2)
@@ -479,6 +486,8 @@ def run_ours(args, world, rank, local):
         mb_ms = e0.elapsed_time(e1) / mb_steps
         mb_bytes = N * (8 * nc * nc + 16 * nc) + F * (8 * t * t + 32 * t)
         mb = {"applies_per_s": 1e3 / mb_ms, "ms_per_apply": mb_ms, "form_s": t_form,
+              "form_kernel_ms": form_ms, "form_gflops": form_flops / form_ms / 1e6,
+              "form_frac_fp64_peak": form_flops / (form_ms * 1e-3) / (fp64_peak_tflops()[0] * 1e12),
               "bytes_per_apply": mb_bytes, "gbs": mb_bytes / (mb_ms * 1e-3) / 1e9}
 
     # ---- full solve (GMRES + D^-1 to 1e-10); the first call allocates the

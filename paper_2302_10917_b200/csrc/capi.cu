@@ -144,6 +144,7 @@ void Knobs::read() {
   if (const char* v = env("MEHDG_ELEM_CH")) elem_ch = atoi(v);
   if (const char* v = env("MEHDG_ELEM_BPOL")) elem_bpol = atoi(v);
   if (const char* v = env("MEHDG_ELEM_LPOL")) elem_lpol = atoi(v);
+  if (const char* v = env("MEHDG_MB_STREAM")) mb_stream = atoi(v);
   if (const char* v = env("MEHDG_MGS_SMALL")) mgs_small = atoi(v);
   if (const char* v = env("MEHDG_MGS_CTAS")) mgs_ctas = std::max(1, atoi(v));
   if (const char* v = env("MEHDG_MGS_REG")) mgs_reg = atoi(v);
@@ -792,7 +793,10 @@ extern "C" int mh_reconstruct_host(mh_system* s, const double* u, double* U) {
 
 extern "C" int mh_form_element_schur(mh_system* s) {
   MH_CHECK(ready(s));
-  MH_CHECK(s->S.alloc((size_t)s->N * s->nc * s->nc));
+  s->ldS = ((int64_t)s->nc * s->nc + kStreamChunk - 1) / kStreamChunk * kStreamChunk;
+  MH_CHECK(s->S.alloc((size_t)s->N * (size_t)s->ldS));
+  if ((int64_t)s->nc * s->nc != s->ldS)  // the per-macro pad is streamed, never used
+    MH_CHECK_CUDA(cudaMemsetAsync(s->S.p, 0, sizeof(double) * (size_t)s->N * (size_t)s->ldS, s->stream));
   MH_CHECK(launch_element_schur(s));
   s->have_mb = true;
   return MH_OK;
@@ -816,8 +820,9 @@ extern "C" int mh_get_element_schur(mh_system* s, int64_t first, int64_t count, 
   }
   const size_t blk = (size_t)s->nc * s->nc;
   if (count)
-    MH_CHECK_CUDA(cudaMemcpyAsync(out, s->S.p + first * blk, sizeof(double) * blk * count,
-                                  cudaMemcpyDeviceToHost, s->stream));
+    MH_CHECK_CUDA(cudaMemcpy2DAsync(out, sizeof(double) * blk, s->S.p + first * s->ldS,
+                                    sizeof(double) * (size_t)s->ldS, sizeof(double) * blk,
+                                    (size_t)count, cudaMemcpyDeviceToHost, s->stream));
   MH_CHECK_CUDA(cudaStreamSynchronize(s->stream));
   // stored transposed as +C A^-1 B; the reference's explicit block is
   // -(C A^-1 B) in row-major order

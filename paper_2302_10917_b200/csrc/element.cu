@@ -197,14 +197,16 @@ element_kernel(ElemArgs a) {
   uint64_t* full = reinterpret_cast<uint64_t*>(rings + (size_t)kWPB * RING);
   uint64_t* empty = full + kWPB * S;
   double* su_all = reinterpret_cast<double*>(empty + kWPB * S);
-  const int nseg = (MODE != kRhs ? 1 : 0) + 2 + (MODE != kRecon ? 1 : 0);
+  const int nseg = MODE == kMb ? 1 : (MODE != kRhs ? 1 : 0) + 2 + (MODE != kRecon ? 1 : 0);
   (void)t;
   if (threadIdx.x == 0) {
     int n = 0;
     if (MODE != kRhs) segs[n++] = Segment{a.Bt, a.ldB, nchB, (MODE == kApply && a.c_is_bt) ? a.bpol : 0};
-    segs[n++] = Segment{a.Lp, a.ldL, nchL, a.lpol};
-    segs[n++] = Segment{a.Up, a.ldL, nchL, a.lpol};
-    if (MODE != kRecon) segs[n++] = Segment{a.Cm, a.ldB, nchB, 0};
+    if (MODE != kMb) {
+      segs[n++] = Segment{a.Lp, a.ldL, nchL, a.lpol};
+      segs[n++] = Segment{a.Up, a.ldL, nchL, a.lpol};
+      if (MODE != kRecon) segs[n++] = Segment{a.Cm, a.ldB, nchB, 0};
+    }
     for (int i = 0; i < 2 * kWPB * S; ++i) mbar_init(&full[i], 1);  // full + empty
     fence_mbar_init();
   }
@@ -224,7 +226,7 @@ element_kernel(ElemArgs a) {
   const uint32_t offL = (MODE != kRhs) ? (uint32_t)a.ldB : 0u;
   const uint32_t offU = offL + (uint32_t)a.ldL;
   const uint32_t offC = offU + (uint32_t)a.ldL;
-  const uint32_t E = offC + ((MODE != kRecon) ? (uint32_t)a.ldB : 0u);
+  const uint32_t E = MODE == kMb ? (uint32_t)a.ldB : offC + ((MODE != kRecon) ? (uint32_t)a.ldB : 0u);
 
   // Software pipeline over a warp's macros: the small per-macro vectors of
   // the NEXT macro (perm, 1/U_jj, face table, gathered uhat) are loaded while
@@ -238,8 +240,8 @@ element_kernel(ElemArgs a) {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int i = lane + 32 * r;
-      pr_n[r] = i < Q ? __ldg(a.perm + en * Q + i) : i;
-      dr_n[r] = i < Q ? __ldg(a.dinv + en * Q + i) : 0.0;
+      pr_n[r] = (MODE != kMb && i < Q) ? __ldg(a.perm + en * Q + i) : i;
+      dr_n[r] = (MODE != kMb && i < Q) ? __ldg(a.dinv + en * Q + i) : 0.0;
     }
 #pragma unroll
 #pragma unroll
@@ -323,6 +325,14 @@ element_kernel(ElemArgs a) {
       }
       __syncwarp();  // su is rewritten for the next macro
       if (en < a.N) gather_next();  // its face table arrived during step 1
+      if (MODE == kMb) {  // explicit element Schur: the rows were S_e^T's, Q = nc
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int i = lane + 32 * r;
+          if (i < Q) a.out[e * Q + i] = acc[r];
+        }
+        continue;
+      }
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         if (MODE == kApply) y[r] = acc[r];
@@ -491,6 +501,38 @@ int launch_rm(mh_system* s, const ElemArgs& a, cudaStream_t st) {
   return launch_rc<R, MODE, MH_ELEM_RING, 512>(s, a, st);
 }
 
+// v = S_e ue through the same stream pipeline: one segment (S_e^T, nc rows of nc)
+int launch_mb(mh_system* s, const double* uhat, double* out, cudaStream_t st) {
+  ElemArgs a{};
+  a.elem_ufac = s->elem_ufac.p;
+  a.uhat = uhat;
+  a.uhalo = s->halo_u.p;
+  a.Bt = s->S.p;
+  a.out = out;
+  a.N = s->N;
+  a.e_lo = 0;
+  a.F = s->F;
+  a.ldB = s->ldS;
+  a.ldL = kStreamChunk;
+  a.Q = s->nc;
+  a.nc = s->nc;
+  a.t = s->t;
+  a.nfe = s->nfe;
+  a.skip = s->skip;
+  switch ((s->nc + 31) / 32) {
+    case 1: return launch_rc<1, kMb, MH_ELEM_RING, 512>(s, a, st);
+    case 2: return launch_rc<2, kMb, MH_ELEM_RING, 512>(s, a, st);
+    case 3: return launch_rc<3, kMb, MH_ELEM_RING, 512>(s, a, st);
+    case 4: return launch_rc<4, kMb, MH_ELEM_RING, 512>(s, a, st);
+    case 5: return launch_rc<5, kMb, MH_ELEM_RING, 512>(s, a, st);
+    case 6: return launch_rc<6, kMb, MH_ELEM_RING, 512>(s, a, st);
+    case 7: return launch_rc<7, kMb, MH_ELEM_RING, 512>(s, a, st);
+    case 8: return launch_rc<8, kMb, MH_ELEM_RING, 512>(s, a, st);
+  }
+  set_error("element kernel: nc > 256 unsupported");
+  return MH_E_UNSUPPORTED;
+}
+
 template <int MODE>
 int launch_mode(mh_system* s, const double* uhat, double* out, cudaStream_t st, int64_t e_lo,
                 int64_t e_hi) {
@@ -551,6 +593,11 @@ int launch_element_range(mh_system* s, int mode, const double* uhat, double* out
   }
   set_error("bad element mode");
   return MH_E_ARG;
+}
+
+int launch_element_mb_stream(mh_system* s, const double* uhat, double* out) {
+  if (s->N == 0) return MH_OK;
+  return launch_mb(s, uhat, out, s->stream);
 }
 
 int launch_element(mh_system* s, int mode, const double* uhat, double* out) {

@@ -79,6 +79,7 @@ struct Knobs {
   int elem_ctas = 0;      // MEHDG_ELEM_CTAS: cap on element-kernel CTAs per SM (0: none)
   int elem_ch = 512;      // MEHDG_ELEM_CH: element stream chunk (doubles)
   int elem_bpol = 1;      // MEHDG_ELEM_BPOL: L2 policy of op.B^T's first read when it is re-read (0 evict_first, 1 evict_last, 2 normal, 3 half evict_last)
+  int mb_stream = 1;      // MEHDG_MB_STREAM: the mb apply through the element kernel's TMA stream
   int elem_lpol = 0;      // MEHDG_ELEM_LPOL: L2 policy of the L / U streams (0 evict_first, 2 normal)
   int mgs_small = 1;      // MEHDG_MGS_SMALL: the MGS block of a step as one kernel
   int mgs_ctas = 4;       // MEHDG_MGS_CTAS: its CTAs per SM (at most)
@@ -125,6 +126,7 @@ struct mh_system {
   mh::DBuf<double> udiag;  // N*Q   diag(U)
   int64_t ldB = 0;         // per-macro stride of Bt / Cm (nc*Q rounded up to kStreamChunk)
   int64_t ldL = 0;         // per-macro stride of Lp / Up (Q(Q-1)/2 rounded up to kStreamChunk)
+  int64_t ldS = 0;         // per-macro stride of S (nc*nc rounded up to kStreamChunk)
   int64_t ldF = 0;         // per-face stride of D / Dinv (t*t rounded up to 16 bytes)
   mh::DBuf<double> dinv;   // N*Q   1/U_ii
   mh::DBuf<int32_t> piv;   // N*Q   LAPACK 0-based pivots
@@ -177,7 +179,7 @@ int launch_occupancy(int device, const void* kern, int threads, size_t smem);
 // lu.cu
 int launch_lu(mh_system* s, float* ms);
 // element.cu
-enum ElemMode { kApply = 0, kRhs = 1, kRecon = 2 };
+enum ElemMode { kApply = 0, kRhs = 1, kRecon = 2, kMb = 3 };  // kMb: v = S_e ue (explicit element Schur)
 int launch_element(mh_system* s, int mode, const double* uhat, double* out);
 // a system with a communicator takes the NCCL path even with one rank (the
 // single-GPU box's test of the NCCL calls); plain systems the no-op path
@@ -187,6 +189,7 @@ int launch_element_range(mh_system* s, int mode, const double* uhat, double* out
                          cudaStream_t st, int64_t e_lo, int64_t e_hi);
 int launch_element_schur(mh_system* s);
 int launch_element_mb(mh_system* s, const double* uhat);
+int launch_element_mb_stream(mh_system* s, const double* uhat, double* out);  // element.cu
 // face.cu
 int launch_face_factor(mh_system* s, const double* Drm);
 int launch_face_reduce(mh_system* s, const double* uhat, double* w, int rhs_mode, int fuse_precond);
