@@ -136,7 +136,9 @@ int launch_occupancy(int device, const void* kern, int threads, size_t smem) {
 
 void Knobs::read() {
   auto env = [](const char* k) { return getenv(k); };
-  if (const char* v = env("MEHDG_LU")) lu = !strcmp(v, "tile") ? 1 : (!strcmp(v, "cta") ? 2 : 0);
+  if (const char* v = env("MEHDG_LU")) lu = !strcmp(v, "tile") ? 1 : (!strcmp(v, "cta") ? 2 : (!strcmp(v, "pipe") ? 3 : 0));
+  if (const char* v = env("MEHDG_LU_PIPE_W")) lu_pipe_w = atoi(v);
+  if (const char* v = env("MEHDG_LU_PIPE_CTAS")) lu_pipe_ctas = atoi(v);
   if (const char* v = env("MEHDG_LU_CTAS")) lu_ctas = std::max(1, atoi(v));
   if (const char* v = env("MEHDG_LU_SCR")) lu_scr_pol = atoi(v);
   if (const char* v = env("MEHDG_LU_APOL")) lu_a_pol = atoi(v);
@@ -193,7 +195,7 @@ extern "C" int mh_destroy(mh_system* s) {
   cudaSetDevice(s->device);
   if (s->stream) cudaStreamSynchronize(s->stream);
   s->elem_ufac.release(); s->face_vslot.release();
-  s->A.release(); s->lu_scr.release(); s->Lp.release(); s->Up.release(); s->udiag.release();
+  s->A.release(); s->lu_scr.release(); s->lu_fb.release(); s->Lp.release(); s->Up.release(); s->udiag.release();
   s->dinv.release(); s->piv.release(); s->perm.release();
   s->lstat.release(); s->Bt.release(); s->Cm.release(); s->Ru.release(); s->D.release();
   s->Draw.release(); s->Rhat.release(); s->Dinv.release(); s->Fkind.release(); s->V.release();

@@ -278,6 +278,10 @@ int launch_lu(mh_system* s, float* ms) {
     // the CTA-resident kernel (lu_cta.cu) measured slower than the warp-per-block
     // tile kernel at every BASELINE shape: selectable, not the default
     MH_CHECK(launch_lu_cta(s, g, e0));
+  } else if (s->knobs.lu == 3 && lu_pipe_supported(Q)) {
+    // one CTA per block, panels pipelined over its warps, L tiles in shared memory;
+    // blocks that need row exchanges come back through the tile kernel (lu_pipe.cu)
+    MH_CHECK(launch_lu_pipe(s, g, e0));
   } else {
     MH_CHECK(launch_lu_tile(s, g, e0));  // records e0 after its scratch allocation
   }

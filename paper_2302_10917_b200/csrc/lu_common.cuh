@@ -23,9 +23,12 @@ struct LuArgs {
   int use_smem;
 };
 
-int launch_lu_tile(mh_system* s, const LuArgs& g, cudaEvent_t start);
+int launch_lu_tile(mh_system* s, const LuArgs& g, cudaEvent_t start, const int64_t* list = nullptr,
+                   const int* list_count = nullptr, int64_t nwork = -1);
+int launch_lu_pipe(mh_system* s, const LuArgs& g, cudaEvent_t start);
 int launch_lu_cta(mh_system* s, const LuArgs& g, cudaEvent_t start);
 bool lu_cta_supported(int Q);
+bool lu_pipe_supported(int Q);
 
 namespace {
 

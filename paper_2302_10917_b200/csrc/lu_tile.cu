@@ -36,103 +36,12 @@
 #include <climits>
 #include <cstdlib>
 
-#include "lu_common.cuh"
+#include "lu_tile_common.cuh"
 
 namespace mh {
 namespace {
 
 constexpr int kTileWarps = 4;
-
-__device__ __forceinline__ void dmma_acc(double& d0, double& d1, double a, double b) {
-  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-      : "+d"(d0), "+d"(d1)
-      : "d"(a), "d"(b));
-}
-
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t p;
-  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-
-// ordered (volatile) load of scratch written earlier in this kernel: it stays
-// behind the previous panel's stores, which also bounds how far the compiler
-// hoists the unrolled update loop's loads (and hence its register use)
-__device__ __forceinline__ double2 ld_v2(const double* ptr, uint64_t pol) {
-  double2 v;
-  asm volatile("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
-               : "=d"(v.x), "=d"(v.y) : "l"(ptr), "l"(pol));
-  return v;
-}
-
-__device__ __forceinline__ void st_v2(double* ptr, double2 v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;"
-               ::"l"(ptr), "d"(v.x), "d"(v.y), "l"(pol));
-}
-
-__device__ __forceinline__ double ld_a(const double* ptr, uint64_t pol) {
-  double v;
-  asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(ptr), "l"(pol));
-  return v;
-}
-
-// L2 priority of the scratch slot (0 normal, 1 evict_last) and of the A stream
-// (0 normal, 1 evict_first): tuning knobs, MEHDG_LU_SCR / MEHDG_LU_APOL
-__device__ __forceinline__ uint64_t make_policy(int kind) {
-  uint64_t p;
-  if (kind == 1) asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  else if (kind == 2) asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  else asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-
-__device__ __forceinline__ void st_first(double* ptr, double v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(ptr), "d"(v), "l"(pol));
-}
-
-// B fragment (rows 4kk..4kk+3 of an 8x8 tile held in C layout):
-// lane l needs element (4kk + l%4, l/4) = lane 4(4kk + l%4) + l/8, register (l/4)&1.
-__device__ __forceinline__ double bfrag(double x0, double x1, int kk, int lane) {
-  const int src = 4 * (4 * kk + (lane & 3)) + (lane >> 3);
-  const double v0 = __shfl_sync(kFull, x0, src);
-  const double v1 = __shfl_sync(kFull, x1, src);
-  return ((lane >> 2) & 1) ? v1 : v0;
-}
-
-// packed-stream offsets in 32-bit arithmetic (Q <= 256)
-__device__ __forceinline__ int ol32(int j, int Q) { return j * (Q - 1) - j * (j - 1) / 2; }
-__device__ __forceinline__ int ou32(int j, int Q) { return Q * (Q - 1) / 2 - j * (j + 1) / 2; }
-
-// scratch tile (kb, t), t >= kb: packed upper-triangular tile index
-__host__ __device__ constexpr int tri(int kb, int t, int nt) {
-  return kb * nt - kb * (kb - 1) / 2 + (t - kb);
-}
-
-__device__ __noinline__ double slow_div(double x, double y) { return x / y; }
-
-__device__ __forceinline__ unsigned hi_abs(double x) {
-  return (unsigned)((uint64_t)__double_as_longlong(x) >> 32) & 0x7fffffffu;
-}
-
-// The reference's test min|U_jj| <= 1e-13 max|A| (schur_solver.py:105-111) from
-// the warp max H of the high words of |a_ij|: max|A| lies in [H:0, H:ffffffff],
-// so the test is decided by the bounds unless dmin falls between them; then the
-// block is re-read for the exact max (practically never).
-__device__ __noinline__ int singular_exact(const double* Ae, int n, double dmin, int lane) {
-  double m = 0.0;
-  for (int i = lane; i < n; i += 32) m = fmax(m, fabs(Ae[i]));
-  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(kFull, m, o));
-  return dmin <= 1e-13 * fmax(m, 1e-300) ? 1 : 0;
-}
-
-__device__ __forceinline__ int singular_test(const double* Ae, int n, unsigned amh, double dmin,
-                                             int lane) {
-  const double lo = __longlong_as_double((long long)((uint64_t)amh << 32));
-  const double hi = __longlong_as_double((long long)(((uint64_t)amh << 32) | 0xffffffffull));
-  if (dmin <= 1e-13 * fmax(lo, 1e-300)) return 1;
-  if (dmin > 1e-13 * fmax(hi, 1e-300)) return 0;
-  return singular_exact(Ae, n, dmin, lane);
-}
 
 template <int NT>
 struct TileShape {
@@ -209,41 +118,57 @@ __device__ __forceinline__ void factor_panel(double* Pw, int* prow, double* Lpe,
 #pragma unroll
   for (int jj = 0; jj < 8; ++jj) {
     if (jj >= ncol) break;
-    // idamax over relative rows jj..nrel-1 (first index on ties): per-lane best,
-    // then the warp max of (hi word + 1, lo word) of |a| and the first position
-    double bv = 0.0, babs = -1.0;
-    int bpos = INT_MAX;
+    // Fast path: idamax takes the first row of maximum |a|, so the diagonal stays
+    // the pivot exactly when no row below it is strictly larger -- one broadcast of
+    // the diagonal, one compare per element, one vote; its reciprocal is already
+    // on its way while the vote resolves.  Otherwise the exact search below.
+    double pv = __shfl_sync(kFull, P[jj][0], jj);
+    int prel = jj;
+    double rcp = __drcp_rn(pv);
+    bool larger = false;
+    {
+      const double apd = fabs(pv);
 #pragma unroll
-    for (int a = 0; a < R; ++a) {
-      const double x = P[jj][a], ax = fabs(x);
-      if ((a > 0 || lane >= jj) && valid[a] && ax > babs) {
-        babs = ax;
-        bv = x;
-        bpos = lane + 32 * a;
+      for (int a = 0; a < R; ++a)
+        if ((a > 0 || lane > jj) && valid[a] && fabs(P[jj][a]) > apd) larger = true;
+    }
+    if (__any_sync(kFull, larger)) {
+      // idamax over relative rows jj..nrel-1 (first index on ties): per-lane best,
+      // then the warp max of (hi word + 1, lo word) of |a| and the first position
+      double bv = 0.0, babs = -1.0;
+      int bpos = INT_MAX;
+#pragma unroll
+      for (int a = 0; a < R; ++a) {
+        const double x = P[jj][a], ax = fabs(x);
+        if ((a > 0 || lane >= jj) && valid[a] && ax > babs) {
+          babs = ax;
+          bv = x;
+          bpos = lane + 32 * a;
+        }
       }
+      const uint64_t bits = (uint64_t)__double_as_longlong(babs);
+      const unsigned khi = babs < 0.0 ? 0u : (unsigned)(bits >> 32) + 1u;
+      const unsigned mhi = __reduce_max_sync(kFull, khi);
+      const unsigned klo = khi == mhi ? (unsigned)bits : 0u;
+      const unsigned mlo = __reduce_max_sync(kFull, klo);
+      prel = (int)__reduce_min_sync(
+          kFull, (unsigned)((khi == mhi && (unsigned)bits == mlo) ? bpos : INT_MAX));
+      pv = __shfl_sync(kFull, bv, prel & 31);
+      if (prel != jj && pv != 0.0) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+#pragma unroll
+          for (int a = 0; a < R; ++a) Pw[c * LDP + lane + 32 * a] = P[c][a];
+        __syncwarp();
+        exchange_rows(Pw, LDP, prow, Lpe, tiles, Q, nt, jb, jj, prel, lane);
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+#pragma unroll
+          for (int a = 0; a < R; ++a) P[c][a] = Pw[c * LDP + lane + 32 * a];
+        __syncwarp();
+      }
+      rcp = __drcp_rn(pv);
     }
-    const uint64_t bits = (uint64_t)__double_as_longlong(babs);
-    const unsigned khi = babs < 0.0 ? 0u : (unsigned)(bits >> 32) + 1u;
-    const unsigned mhi = __reduce_max_sync(kFull, khi);
-    const unsigned klo = khi == mhi ? (unsigned)bits : 0u;
-    const unsigned mlo = __reduce_max_sync(kFull, klo);
-    const int prel = (int)__reduce_min_sync(
-        kFull, (unsigned)((khi == mhi && (unsigned)bits == mlo) ? bpos : INT_MAX));
-    const double pv = __shfl_sync(kFull, bv, prel & 31);
-    if (prel != jj && pv != 0.0) {
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-#pragma unroll
-        for (int a = 0; a < R; ++a) Pw[c * LDP + lane + 32 * a] = P[c][a];
-      __syncwarp();
-      exchange_rows(Pw, LDP, prow, Lpe, tiles, Q, nt, jb, jj, prel, lane);
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-#pragma unroll
-        for (int a = 0; a < R; ++a) P[c][a] = Pw[c * LDP + lane + 32 * a];
-      __syncwarp();
-    }
-    const double rcp = __drcp_rn(pv);
     if (pv != 0.0) {
       if (fabs(pv) >= DBL_MIN) {
 #pragma unroll
@@ -291,28 +216,10 @@ __device__ __forceinline__ void factor_panel(double* Pw, int* prow, double* Lpe,
   __syncwarp();
 }
 
-// -L11^-1 of the panel's unit-lower diagonal block (rows 0..7 of Pw) in
-// A-fragment order: element (rr, j) -> dst[2 (4 rr + j % 4) + j / 4].  Lanes 0..7.
-template <int LDP>
-__device__ __forceinline__ void neg_linv(const double* Pw, double* dst, int lane) {
-  if (lane < 8) {
-    const int jcol = lane;
-    double x[8];
-#pragma unroll
-    for (int rr = 0; rr < 8; ++rr) {
-      double s = 0.0;
-#pragma unroll
-      for (int m = 0; m < rr; ++m) s = fma(-Pw[m * LDP + rr], x[m], s);
-      x[rr] = rr < jcol ? 0.0 : (rr == jcol ? 1.0 : s);
-      dst[2 * (4 * rr + (jcol & 3)) + (jcol >> 2)] = -x[rr];
-    }
-  }
-  __syncwarp();
-}
-
 template <int NT>
 __global__ void __launch_bounds__(kTileWarps * 32, TileShape<NT>::kMinBlocks)
-    lu_tile_kernel(LuArgs g, double* __restrict__ scr, int scr_pol, int a_pol) {
+    lu_tile_kernel(LuArgs g, double* __restrict__ scr, int scr_pol, int a_pol,
+                   const int64_t* __restrict__ list, const int* __restrict__ list_count) {
   using S = TileShape<NT>;
   constexpr int R = S::R, LDP = S::LDP;
   extern __shared__ double smem_tile[];
@@ -329,7 +236,11 @@ __global__ void __launch_bounds__(kTileWarps * 32, TileShape<NT>::kMinBlocks)
   const uint64_t pol = policy_evict_first();
   const uint64_t spol = make_policy(scr_pol), apol = make_policy(a_pol ? 2 : 0);
 
-  for (int64_t e = wid; e < g.nblocks; e += (int64_t)gridDim.x * kTileWarps) {
+  // with a list (the blocks the pipelined kernel handed back, lu_pipe.cu) the
+  // grid walks list[0 .. *list_count)
+  const int64_t nwork = list ? (int64_t)*list_count : g.nblocks;
+  for (int64_t it = wid; it < nwork; it += (int64_t)gridDim.x * kTileWarps) {
+    const int64_t e = list ? list[it] : it;
     const double* __restrict__ Ae = g.A + e * (int64_t)Q * Q;
     double* Lpe = g.Lp + e * g.ldL;
     double* Upe = g.Up + e * g.ldL;
@@ -429,7 +340,8 @@ __global__ void __launch_bounds__(kTileWarps * 32, TileShape<NT>::kMinBlocks)
 }
 
 template <int NT>
-int launch_nt(mh_system* s, const LuArgs& g, cudaEvent_t start) {
+int launch_nt(mh_system* s, const LuArgs& g, cudaEvent_t start, const int64_t* list,
+              const int* list_count, int64_t nwork) {
   using S = TileShape<NT>;
   const size_t smem = S::smem_bytes();
   MH_CHECK_CUDA(cudaFuncSetAttribute(lu_tile_kernel<NT>,
@@ -442,11 +354,12 @@ int launch_nt(mh_system* s, const LuArgs& g, cudaEvent_t start) {
   // hide more latency but their scratch slots crowd L2 (MEHDG_LU_CTAS overrides)
   per_sm = std::max(1, std::min(per_sm, s->knobs.lu_ctas));
   const int scr_pol = s->knobs.lu_scr_pol, a_pol = s->knobs.lu_a_pol;
-  const int64_t need = (g.nblocks + kTileWarps - 1) / kTileWarps;
+  const int64_t need = (nwork + kTileWarps - 1) / kTileWarps;
   const int64_t grid = std::min<int64_t>(need, (int64_t)per_sm * s->num_sms);
-  MH_CHECK(s->lu_scr.alloc((size_t)grid * kTileWarps * S::kSlotDoubles));
+  MH_CHECK(s->lu_scr.ensure((size_t)grid * kTileWarps * S::kSlotDoubles));
   if (start) MH_CHECK_CUDA(cudaEventRecord(start, s->stream));
-  lu_tile_kernel<NT><<<(unsigned)grid, kTileWarps * 32, smem, s->stream>>>(g, s->lu_scr.p, scr_pol, a_pol);
+  lu_tile_kernel<NT><<<(unsigned)grid, kTileWarps * 32, smem, s->stream>>>(g, s->lu_scr.p, scr_pol, a_pol,
+                                                                             list, list_count);
   MH_CHECK_CUDA(cudaGetLastError());
   return MH_OK;
 }
@@ -455,10 +368,14 @@ int launch_nt(mh_system* s, const LuArgs& g, cudaEvent_t start) {
 
 // Q in 33..256: NT = ceil(Q / 8) tiles, instantiated for the BASELINE shapes
 // (Q = 84, 91, 165, 220 -> NT = 11, 12, 21, 28) and a few sizes between.
-int launch_lu_tile(mh_system* s, const LuArgs& g, cudaEvent_t start) {
+// `list` / `list_count` (device) / `nwork` (host copy of the count): factor only
+// the listed blocks; nullptr / nullptr / -1: all of them.
+int launch_lu_tile(mh_system* s, const LuArgs& g, cudaEvent_t start, const int64_t* list,
+                   const int* list_count, int64_t nwork) {
+  if (nwork < 0) nwork = g.nblocks;
   const int nt = (g.Q + 7) / 8;
 #define MH_NT(N) \
-  if (nt <= N) return launch_nt<N>(s, g, start);
+  if (nt <= N) return launch_nt<N>(s, g, start, list, list_count, nwork);
   MH_NT(6) MH_NT(8) MH_NT(10) MH_NT(11) MH_NT(12) MH_NT(14) MH_NT(16) MH_NT(18) MH_NT(21)
   MH_NT(24) MH_NT(28) MH_NT(32)
 #undef MH_NT

@@ -72,7 +72,9 @@ struct Krylov;  // GMRES workspace (krylov.cu)
 // Tuning knobs: read from the environment once, when a
 // system is created, never on a launch path.  Defaults are the measured best.
 struct Knobs {
-  int lu = 0;             // MEHDG_LU: 0 default, 1 tile, 2 cta
+  int lu = 0;             // MEHDG_LU: 0 default (pipe where it fits), 1 tile, 2 cta, 3 pipe
+  int lu_pipe_w = 0;      // MEHDG_LU_PIPE_W: warps per block of the pipelined LU (0: by size)
+  int lu_pipe_ctas = 0;   // MEHDG_LU_PIPE_CTAS: cap on its CTAs per SM (0: none)
   int lu_ctas = 3;        // MEHDG_LU_CTAS: resident CTAs per SM of the tile LU
   int lu_scr_pol = 0;     // MEHDG_LU_SCR: L2 policy of the tile LU's scratch
   int lu_a_pol = 1;       // MEHDG_LU_APOL: L2 policy of the A stream (1 evict_first)
@@ -121,6 +123,8 @@ struct mh_system {
   // blocks
   mh::DBuf<double> A;      // staged A, N*Q*Q row-major (input of the LU)
   mh::DBuf<double> lu_scr; // per-warp-slot scratch of the tile LU (inverse diagonal blocks)
+  mh::DBuf<int64_t> lu_fb; // pipelined LU: [0] count, [1..] blocks handed to the tile kernel
+  int lu_fallback_blocks = 0;  // how many the last factorisation handed over
   mh::DBuf<double> Lp;     // N*ldL packed strict lower L, columns 0..Q-2 (streamed)
   mh::DBuf<double> Up;     // N*ldL packed strict upper U, columns Q-1..1 (streamed)
   mh::DBuf<double> udiag;  // N*Q   diag(U)

@@ -60,10 +60,12 @@ def gpu():
     return 0
 
 
-@pytest.fixture(params=["default", "cta"])
+@pytest.fixture(params=["default", "cta", "pipe"])
 def lu_kernel(request, monkeypatch):
-    """The default batched LU and the CTA-resident one (csrc/lu_cta.cu, 32 < Q <= 168),
-    chosen by MEHDG_LU when a system is factorized."""
-    if request.param == "cta":
-        monkeypatch.setenv("MEHDG_LU", "cta")
+    """The default batched LU, the CTA-resident one (csrc/lu_cta.cu, 32 < Q <= 168) and
+    the pipelined one (csrc/lu_pipe.cu, 32 < Q <= 224; blocks that need row exchanges
+    come back through the default kernel), chosen by MEHDG_LU when a system is
+    factorized."""
+    if request.param != "default":
+        monkeypatch.setenv("MEHDG_LU", request.param)
     return request.param

@@ -38,6 +38,8 @@ def problem_with_blocks(Q, seed):
 def test_lu_matches_lapack_across_sizes(Q, lu_kernel):
     if lu_kernel == "cta" and not 32 < Q <= 168:
         pytest.skip("the CTA-resident LU covers 32 < Q <= 168")
+    if lu_kernel == "pipe" and not 32 < Q <= 224:
+        pytest.skip("the pipelined LU covers 32 < Q <= 224")
     prob = problem_with_blocks(Q, seed=100 + Q)
     tables = {"nfe": 3, "elem_ufac": prob["elem_face"], "face_elem": prob["face_elem"],
               "face_slot": prob["face_slot"], "uidx": prob["uidx"], "F": prob["F"]}
