@@ -153,24 +153,41 @@ __device__ __forceinline__ void form_bwd(double (&X)[NT][2], const FormCtx& c) {
   }
 }
 
-template <int NT, int KB>
+// C's A fragments of row-tile step KB for the kFormGroup output tiles from g0
+template <int NT>
+__device__ __forceinline__ void form_cy_load(double (&a)[kFormGroup][2], int KB, int g0,
+                                             const FormCtx& c) {
+  const int i0 = 8 * KB + c.q, i1 = i0 + 4;
+#pragma unroll
+  for (int g = 0; g < kFormGroup; ++g) {
+    const int cp = 8 * (g0 + g) + c.r;
+    a[g][0] = (KB < c.nt && cp < c.nc && i0 < c.Q) ? __ldg(c.Ce + (size_t)cp * c.Q + i0) : 0.0;
+    a[g][1] = (KB < c.nt && cp < c.nc && i1 < c.Q) ? __ldg(c.Ce + (size_t)cp * c.Q + i1) : 0.0;
+  }
+}
+
+// acc(g) += C(tile g0 + g, k) Y_k over the row tiles k; the next step's C
+// fragments are loaded before this step's DMMAs
+template <int NT>
 __device__ __forceinline__ void form_cy(const double (&X)[NT][2], double (&acc)[kFormGroup][2],
                                         int g0, const FormCtx& c) {
-  if constexpr (KB < NT) {
+  // (two CTAs per SM for NT <= 12: 128 registers, no room for the second buffer)
+  constexpr bool kAhead = NT > 12;
+  double a[kAhead ? 2 : 1][kFormGroup][2];
+  if (kAhead) form_cy_load<NT>(a[0], 0, g0, c);
+#pragma unroll
+  for (int KB = 0; KB < NT; ++KB) {
+    if (!kAhead) form_cy_load<NT>(a[0], KB, g0, c);
+    else if (KB + 1 < NT) form_cy_load<NT>(a[(KB + 1) & 1], KB + 1, g0, c);
     if (KB < c.nt) {
       const double yb0 = bfrag_of_c(X[KB][0], X[KB][1], 0, c.lane);
       const double yb1 = bfrag_of_c(X[KB][0], X[KB][1], 1, c.lane);
-      const int i0 = 8 * KB + c.q, i1 = i0 + 4;
 #pragma unroll
       for (int g = 0; g < kFormGroup; ++g) {
-        const int cp = 8 * (g0 + g) + c.r;
-        const double a0 = (cp < c.nc && i0 < c.Q) ? __ldg(c.Ce + (size_t)cp * c.Q + i0) : 0.0;
-        const double a1 = (cp < c.nc && i1 < c.Q) ? __ldg(c.Ce + (size_t)cp * c.Q + i1) : 0.0;
-        dmma(acc[g][0], acc[g][1], a0, yb0);
-        dmma(acc[g][0], acc[g][1], a1, yb1);
+        dmma(acc[g][0], acc[g][1], a[kAhead ? (KB & 1) : 0][g][0], yb0);
+        dmma(acc[g][0], acc[g][1], a[kAhead ? (KB & 1) : 0][g][1], yb1);
       }
     }
-    form_cy<NT, KB + 1>(X, acc, g0, c);
   }
 }
 
@@ -184,8 +201,20 @@ __device__ __forceinline__ void stage_lower(double* tiles, const double* Le, int
     const int kb = j >> 3, cj = j & 7;
     double* tc = tiles + (FormCfg<NT>::ltiles(K0, kb) - kb - 1) * 64 + (cj >> 2) * 32 + (cj & 3);
     const double* col = Le + off_lower(j, Q) - (j + 1);
-    for (int i = 8 * (kb + 1) + lane; i < 8 * NT; i += 32)
-      tc[(i >> 3) * 64 + (i & 7) * 4] = (i < Q && j < Q) ? -__ldg(col + i) : 0.0;
+    // all of the column's loads first, then the stores (the loads of a plain loop
+    // wait for one another behind the shared-memory stores)
+    constexpr int NI = (8 * NT + 31) / 32;
+    double v[NI];
+#pragma unroll
+    for (int k = 0; k < NI; ++k) {
+      const int i = 8 * (kb + 1) + lane + 32 * k;
+      v[k] = (i < Q && j < Q) ? -__ldg(col + i) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < NI; ++k) {
+      const int i = 8 * (kb + 1) + lane + 32 * k;
+      if (i < 8 * NT) tc[(i >> 3) * 64 + (i & 7) * 4] = v[k];
+    }
   }
 }
 
@@ -197,8 +226,18 @@ __device__ __forceinline__ void stage_upper(double* tiles, const double* Ue, int
     const int kb = j >> 3, cj = j & 7;
     double* tc = tiles + FormCfg<NT>::utiles(K0, kb) * 64 + (cj >> 2) * 32 + (cj & 3);
     const double* col = Ue + off_upper(j, Q);
-    for (int i = lane; i < 8 * kb; i += 32)
-      tc[(i >> 3) * 64 + (i & 7) * 4] = j < Q ? -__ldg(col + i) : 0.0;
+    constexpr int NI = (8 * NT + 31) / 32;
+    double v[NI];
+#pragma unroll
+    for (int k = 0; k < NI; ++k) {
+      const int i = lane + 32 * k;
+      v[k] = (i < 8 * kb && j < Q) ? -__ldg(col + i) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < NI; ++k) {
+      const int i = lane + 32 * k;
+      if (i < 8 * kb) tc[(i >> 3) * 64 + (i & 7) * 4] = v[k];
+    }
   }
 }
 
@@ -305,7 +344,7 @@ __global__ void __launch_bounds__(256, NT <= 12 ? 2 : 1) form_dmma_kernel(FormAr
     double acc[kFormGroup][2];
 #pragma unroll
     for (int g = 0; g < kFormGroup; ++g) acc[g][0] = acc[g][1] = 0.0;
-    form_cy<NT, 0>(X, acc, g0, ctx);
+    form_cy<NT>(X, acc, g0, ctx);
 #pragma unroll
     for (int g = 0; g < kFormGroup; ++g) {
       const int cp = 8 * (g0 + g) + r;
