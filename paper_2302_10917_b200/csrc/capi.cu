@@ -147,6 +147,8 @@ void Knobs::read() {
   if (const char* v = env("MEHDG_ELEM_BPOL")) elem_bpol = atoi(v);
   if (const char* v = env("MEHDG_ELEM_LPOL")) elem_lpol = atoi(v);
   if (const char* v = env("MEHDG_MB_STREAM")) mb_stream = atoi(v);
+  if (const char* v = env("MEHDG_ELEM_SPLIT")) elem_split = atoi(v);
+  if (const char* v = env("MEHDG_ELEM_SPLIT_CTAS")) elem_split_ctas = atoi(v);
   if (const char* v = env("MEHDG_MGS_SMALL")) mgs_small = atoi(v);
   if (const char* v = env("MEHDG_MGS_CTAS")) mgs_ctas = std::max(1, atoi(v));
   if (const char* v = env("MEHDG_MGS_REG")) mgs_reg = atoi(v);

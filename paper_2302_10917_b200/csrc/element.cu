@@ -29,6 +29,7 @@
 // around the ring end is read with immediate-offset shared loads.
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "mh_internal.h"
@@ -501,6 +502,8 @@ int launch_rm(mh_system* s, const ElemArgs& a, cudaStream_t st) {
   return launch_rc<R, MODE, MH_ELEM_RING, 512>(s, a, st);
 }
 
+#include "element_split.cuh"
+
 // v = S_e ue through the same stream pipeline: one segment (S_e^T, nc rows of nc)
 int launch_mb(mh_system* s, const double* uhat, double* out, cudaStream_t st) {
   ElemArgs a{};
@@ -562,6 +565,9 @@ int launch_mode(mh_system* s, const double* uhat, double* out, cudaStream_t st, 
   a.bpol = s->knobs.elem_bpol;
   a.lpol = s->knobs.elem_lpol;
   a.skip = MODE == kApply ? s->skip : nullptr;
+  // apply mode with op.C = op.B^T and three or more row groups: the macro split
+  // over its row groups, few macros in flight (MEHDG_ELEM_SPLIT)
+  if (MODE == kApply && s->knobs.elem_split && s->c_is_bt && s->Q > 64) return launch_split(s, a, st);
   switch ((s->Q + 31) / 32) {
     case 1: return launch_rm<1, MODE>(s, a, st);
     case 2: return launch_rm<2, MODE>(s, a, st);

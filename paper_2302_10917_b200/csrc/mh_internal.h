@@ -81,6 +81,8 @@ struct Knobs {
   int elem_ctas = 0;      // MEHDG_ELEM_CTAS: cap on element-kernel CTAs per SM (0: none)
   int elem_ch = 512;      // MEHDG_ELEM_CH: element stream chunk (doubles)
   int elem_bpol = 1;      // MEHDG_ELEM_BPOL: L2 policy of op.B^T's first read when it is re-read (0 evict_first, 1 evict_last, 2 normal, 3 half evict_last)
+  int elem_split = 0;      // MEHDG_ELEM_SPLIT: apply-mode element kernel with a macro split over its row groups
+  int elem_split_ctas = 0; // MEHDG_ELEM_SPLIT_CTAS: its CTAs (macros in flight) per SM (0: by L2 footprint)
   int mb_stream = 1;      // MEHDG_MB_STREAM: the mb apply through the element kernel's TMA stream
   int elem_lpol = 0;      // MEHDG_ELEM_LPOL: L2 policy of the L / U streams (0 evict_first, 2 normal)
   int mgs_small = 1;      // MEHDG_MGS_SMALL: the MGS block of a step as one kernel

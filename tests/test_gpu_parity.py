@@ -427,3 +427,28 @@ def test_host_factors_and_solve_driver(gpu):
     assert 0.0 < rec["t_local_s"] and rec["t_global_s"] >= 0.0
     assert rel(sol.uhat, g["x"]) <= SOLVE_TOL
     assert rel(np.stack(sol.local), g["U"]) <= SOLVE_TOL
+
+
+@pytest.mark.parametrize("d,n,m,p", [(3, 2, 2, 3), (2, 4, 4, 3), (3, 2, 2, 4), (3, 1, 3, 3),
+                                     (2, 3, 2, 5)])
+@pytest.mark.parametrize("kind", ["dd", "gauss"])
+def test_split_element_kernel_matches(gpu, d, n, m, p, kind, monkeypatch):
+    """The apply with a macro split over its row groups (csrc/element_split.cuh,
+    MEHDG_ELEM_SPLIT=1; Q = 84, 91, 165, 220, 66) equals the warp-per-macro kernel
+    (same substitution order: 1e-14) and the oracle, with and without row
+    permutations; a solve through it converges to the same solution."""
+    prob = S.make_problem(d, n, m, p, seed=21)
+    if kind == "gauss":
+        prob["A"] = np.random.default_rng(5).standard_normal(prob["A"].shape)
+    sys0, cfg = condense_problem(prob)
+    w0 = P.apply_schur(sys0, prob["uhat"])
+    monkeypatch.setenv("MEHDG_ELEM_SPLIT", "1")
+    sys1, _ = condense_problem(prob)
+    w1 = P.apply_schur(sys1, prob["uhat"])
+    assert rel(w1, w0) <= 1e-14
+    if kind == "dd":
+        o = SO.system_from_problem(prob).factorize()
+        assert rel(w1, o.apply(prob["uhat"])) <= APPLY_TOL
+        x1, info = P.gmres(P.SchurOperator(sys1), sys1.f_vec, cfg, precond=P.Preconditioner(sys1))
+        x0, _ = P.gmres(P.SchurOperator(sys0), sys0.f_vec, cfg, precond=P.Preconditioner(sys0))
+        assert info["converged"] and rel(x1, x0) <= SOLVE_TOL
