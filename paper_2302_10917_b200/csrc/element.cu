@@ -35,6 +35,10 @@
 #include "mh_internal.h"
 #include "stream.cuh"
 
+// the kMb instantiations leave the macro loop body after step 1 (`continue`): the
+// steps behind it are unreachable there by design
+#pragma nv_diag_suppress 128
+
 namespace mh {
 namespace {
 
