@@ -6,6 +6,7 @@
 
 __global__ void probe(double* out, long long* cyc, double seed) {
   const int lane = threadIdx.x;
+  __shared__ double sm[32];
   double x = seed + lane * 1e-3;
   unsigned u = (unsigned)lane;
   long long t0, t1;
@@ -29,6 +30,14 @@ __global__ void probe(double* out, long long* cyc, double seed) {
     x = __longlong_as_double((long long)(b ^ 1ull));
   })
   TIME(10, x = __ddiv_rn(1.0, x))
+  // the substitution / pivot chains alternate pipes: fp64 result -> shuffle -> fp64
+  TIME(11, x = __shfl_sync(0xffffffffu, fma(x, 0.999, 1e-9), (lane + 1) & 31))
+  TIME(12, {
+    sm[lane] = fma(x, 0.999, 1e-9);
+    __syncwarp();
+    x = sm[(lane + 1) & 31];
+    __syncwarp();
+  })
   out[lane] = x + u;
 }
 
@@ -42,7 +51,8 @@ int main() {
   cudaDeviceSynchronize();
   const char* names[] = {"DFMA", "DMUL", "DADD", "fabs>? sel (DSETP+FSEL+DADD)", "drcp_rn",
                          "REDUX.MAX +IADD", "SHFL.IDX f64", "VOTE.ballot +IADD", "IMAD",
-                         "LOP xor (64-bit as 2x32)", "ddiv_rn"};
-  for (int k = 0; k < 11; ++k) printf("%-32s %6.1f cyc/op\n", names[k], cyc[k] / 256.0);
+                         "LOP xor (64-bit as 2x32)", "ddiv_rn", "DFMA -> SHFL.IDX f64 (chain)",
+                         "DFMA -> STS / LDS f64 (chain)"};
+  for (int k = 0; k < 13; ++k) printf("%-32s %6.1f cyc/op\n", names[k], cyc[k] / 256.0);
   return 0;
 }
