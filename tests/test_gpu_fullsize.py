@@ -12,7 +12,10 @@ covered):
 * the GMRES solve (schur_solver.py:308-385): converged, its preconditioned
   residual <= tol through the device operator, and the slab oracle's own
   residual on the complete faces consistent with it;
-* bitwise determinism of a second apply at full size.
+* bitwise determinism of a second apply at full size;
+* the matrix-based mode at full size (schur_solver.py:388-420): S_e formed on the
+  device for every macro, its apply equal to the matrix-free one to 1e-12 (64-bit
+  offsets of the padded S_e stream, every right-hand-side group of the form kernel).
 
 The oracle is pinned to the reference at c1-c3 (tests/test_oracle_golden.py).
 Host memory: c4 holds ~70 GB of blocks; the test skips on smaller hosts.
@@ -75,6 +78,8 @@ def test_full_size_against_oracle_slabs(gpu, name):
     assert np.linalg.norm(r) <= 10 * cfg.tol * Mf
     del x
     torch.cuda.empty_cache()
+    P.form_element_schur(sys_)
+    assert rel(P.apply_schur_mb(sys_, uhat), w) <= APPLY_TOL, f"{name}: matrix-based apply"
 
     slab = 6 * n * n  # one x-slab of Kuhn tets (mesh.py:407-417)
     for e0 in (0, (n // 2) * slab, N - slab):
